@@ -1,0 +1,483 @@
+// K2 + K3 + K4a: fused per-edge reprojection / Jacobians / whitened Gram,
+// deterministic segmented reductions into the block-sparse normal equations,
+// and the Schur elimination of the inverse depths.
+//
+// Restates ba.residuals/objective (ba.py:219-253) and ba.assemble
+// (ba.py:328-440) with geometry.reproject_grid (geometry.py:478-529) inlined.
+// Every reduction runs over a fixed, index-sorted list (no float atomics), so
+// results are bit-identical run to run.
+#include "problem.cuh"
+
+namespace dpv {
+namespace {
+
+struct Frame {
+    double R[9];
+    double t[3];
+};
+
+__device__ __forceinline__ void load_frame(const double* Rall, const double* tall, int f,
+                                           Frame& fr) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) fr.R[k] = __ldg(Rall + 9 * f + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) fr.t[k] = __ldg(tall + 3 * f + k);
+}
+
+// One patch cell: world point, target-camera point, validity and pixel.
+struct Cell {
+    double xw[3];
+    double xt[3];
+    double zs;
+    bool valid;
+    double u, v;
+};
+
+__device__ __forceinline__ void reproject_cell(double rx, double ry, double inv_d_recip,
+                                               const Frame& fi, const Frame& fj,
+                                               const double* intr, Cell& c) {
+    // x_cam = ray / d  (ray z = 1)
+    const double xc0 = rx * inv_d_recip, xc1 = ry * inv_d_recip, xc2 = inv_d_recip;
+    // x_w = R_i x_c + t_i
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        c.xw[r] = fi.R[3 * r] * xc0 + fi.R[3 * r + 1] * xc1 + fi.R[3 * r + 2] * xc2 + fi.t[r];
+    const double e0 = c.xw[0] - fj.t[0], e1 = c.xw[1] - fj.t[1], e2 = c.xw[2] - fj.t[2];
+    // x_t = R_j^T (x_w - t_j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c.xt[k] = fj.R[k] * e0 + fj.R[3 + k] * e1 + fj.R[6 + k] * e2;
+    c.valid = c.xt[2] > kDepthEps;
+    c.zs = c.valid ? c.xt[2] : 1.0;
+    c.u = intr[0] * c.xt[0] / c.zs + intr[2];
+    c.v = intr[1] * c.xt[1] / c.zs + intr[3];
+}
+
+// ---------------------------------------------------------------------------
+// K2 objective: sum_e sum_cells w_comp * valid * r^2 (ba.py:248-253)
+
+__global__ void __launch_bounds__(256) k_objective(
+    int64_t E, int m, int64_t P, const int32_t* __restrict__ a_src,
+    const int32_t* __restrict__ a_dst, const int32_t* __restrict__ a_row,
+    const double* __restrict__ a_tgt, const double* __restrict__ a_w,
+    const double* __restrict__ r_ray, const double* __restrict__ Rall,
+    const double* __restrict__ tall, const double* __restrict__ d, double fx, double fy,
+    double cx, double cy, double* __restrict__ part) {
+    const double intr[4] = {fx, fy, cx, cy};
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        Frame fi, fj;
+        load_frame(Rall, tall, a_src[e], fi);
+        load_frame(Rall, tall, a_dst[e], fj);
+        const int32_t row = a_row[e];
+        const double id = 1.0 / __ldg(d + row);
+        const double w0 = a_w[e], w1 = a_w[E + e];
+        double s = 0.0;
+        for (int c = 0; c < m; ++c) {
+            Cell cl;
+            reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
+                           __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr, cl);
+            if (cl.valid) {
+                const double r0 = cl.u - a_tgt[(int64_t)(2 * c) * E + e];
+                const double r1 = cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e];
+                s += w0 * r0 * r0 + w1 * r1 * r1;
+            }
+        }
+        acc += s;
+    }
+    // fixed-order block reduction
+    __shared__ double sh[8];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_sum_parts(int n, const double* part, double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        out[0] = t;
+    }
+}
+
+// residual export in problem-edge order (ba.py:219-245)
+__global__ void k_residuals(int64_t E, int m, int64_t P, const int32_t* a_src,
+                            const int32_t* a_dst, const int32_t* a_row, const int32_t* a_pidx,
+                            const double* a_tgt, const double* r_ray, const double* Rall,
+                            const double* tall, const double* d, double fx, double fy, double cx,
+                            double cy, double* res, uint8_t* valid) {
+    const double intr[4] = {fx, fy, cx, cy};
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        Frame fi, fj;
+        load_frame(Rall, tall, a_src[e], fi);
+        load_frame(Rall, tall, a_dst[e], fj);
+        const int32_t row = a_row[e];
+        const double id = 1.0 / d[row];
+        const int64_t p = a_pidx[e];
+        for (int c = 0; c < m; ++c) {
+            Cell cl;
+            reproject_cell(r_ray[(int64_t)(2 * c) * P + row], r_ray[(int64_t)(2 * c + 1) * P + row],
+                           id, fi, fj, intr, cl);
+            res[(p * m + c) * 2] = cl.u - a_tgt[(int64_t)(2 * c) * E + e];
+            res[(p * m + c) * 2 + 1] = cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e];
+            valid[p * m + c] = cl.valid ? 1 : 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2+K3 fused: one warp per segment (same source/target frame, <= kSegMax
+// edges), one lane per edge.  Per edge it writes e_pd (6), c_dd, g_d; per
+// segment the warp-reduced sum of J^T W J (21, upper) and J^T W r (6).
+
+__device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
+    return a * 6 - (a * (a - 1)) / 2 + (b - a);
+}
+
+__global__ void __launch_bounds__(128) k_assemble_edges(
+    int64_t S, int64_t E, int m, int64_t P, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
+    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
+    const double* __restrict__ a_w, const double* __restrict__ r_ray,
+    const double* __restrict__ Rall, const double* __restrict__ tall,
+    const double* __restrict__ d, double fx, double fy, double cx, double cy,
+    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g) {
+    const double intr[4] = {fx, fy, cx, cy};
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = warp; s < S; s += nwarps) {
+        const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
+        Frame fi, fj;
+        load_frame(Rall, tall, seg_src[s], fi);
+        load_frame(Rall, tall, seg_dst[s], fj);
+        double H[21], G[6];
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) G[k] = 0.0;
+        for (int32_t e = e0 + lane; e < e1; e += 32) {
+            const int32_t row = a_row[e];
+            const double dd = __ldg(d + row);
+            const double id = 1.0 / dd;
+            const double sw0 = sqrt(a_w[e]), sw1 = sqrt(a_w[E + e]);
+            double ep[6] = {0, 0, 0, 0, 0, 0};
+            double cdd = 0.0, gd = 0.0;
+            for (int c = 0; c < m; ++c) {
+                Cell cl;
+                reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
+                               __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr,
+                               cl);
+                const double s0 = cl.valid ? sw0 : 0.0;
+                const double s1 = cl.valid ? sw1 : 0.0;
+                const double iz = 1.0 / cl.zs;
+                // A = Jproj R_j^T (geometry.py:514-522)
+                const double p0 = intr[0] * iz, q0 = -intr[0] * cl.xt[0] * iz * iz;
+                const double p1 = intr[1] * iz, q1 = -intr[1] * cl.xt[1] * iz * iz;
+                double J[2][6], jd[2];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    J[0][k] = p0 * fj.R[3 * k] + q0 * fj.R[3 * k + 2];
+                    J[1][k] = p1 * fj.R[3 * k + 1] + q1 * fj.R[3 * k + 2];
+                }
+                // rotational part x_w x a_row (geometry.py:524-526)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    J[r][3] = cl.xw[1] * J[r][2] - cl.xw[2] * J[r][1];
+                    J[r][4] = cl.xw[2] * J[r][0] - cl.xw[0] * J[r][2];
+                    J[r][5] = cl.xw[0] * J[r][1] - cl.xw[1] * J[r][0];
+                }
+                // depth: A (t_i - x_w) / d (geometry.py:527-528)
+                const double g0 = (fi.t[0] - cl.xw[0]) * id, g1 = (fi.t[1] - cl.xw[1]) * id,
+                             g2 = (fi.t[2] - cl.xw[2]) * id;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) jd[r] = J[r][0] * g0 + J[r][1] * g1 + J[r][2] * g2;
+                const double rr[2] = {(cl.u - a_tgt[(int64_t)(2 * c) * E + e]) ,
+                                      (cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e])};
+                const double sw[2] = {s0, s1};
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    double jw[6];
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) jw[k] = J[r][k] * sw[r];
+                    const double jdw = jd[r] * sw[r];
+                    const double rw = rr[r] * sw[r];
+#pragma unroll
+                    for (int a = 0; a < 6; ++a) {
+#pragma unroll
+                        for (int b = a; b < 6; ++b) H[utri(a, b)] += jw[a] * jw[b];
+                        G[a] += jw[a] * rw;
+                        ep[a] += jw[a] * jdw;
+                    }
+                    cdd += jdw * jdw;
+                    gd += jdw * rw;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 6; ++k) e_terms[(int64_t)k * E + e] = ep[k];
+            e_terms[6 * E + e] = cdd;
+            e_terms[7 * E + e] = gd;
+        }
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
+        if (lane < 21) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < 21; ++k) v = (lane == k) ? H[k] : v;
+            seg_h[s * 21 + lane] = v;
+        }
+        if (lane < 6) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
+            seg_g[s * 6 + lane] = v;
+        }
+    }
+}
+
+// depth side (ba.py:370-373): per-row sums over the row's edges
+__global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32_t* row_pos,
+                       const double* e_terms, double* depth_diag, double* rhs_depth,
+                       uint8_t* active, double* cinv0, unsigned long long* grad_bits,
+                       unsigned long long* n_inactive) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double c = 0.0, g = 0.0;
+        for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+            const int32_t e = row_pos[k];
+            c += e_terms[6 * E + e];
+            g += e_terms[7 * E + e];
+        }
+        depth_diag[r] = c;
+        rhs_depth[r] = -g;
+        const bool act = c > kActiveEps;
+        active[r] = act ? 1 : 0;
+        cinv0[r] = act ? 1.0 / c : 0.0;
+        if (act) atomicMax(grad_bits, (unsigned long long)__double_as_longlong(fabs(g)));
+        else atomicAdd(n_inactive, 1ull);
+    }
+}
+
+// coupling blocks per (var, row) incidence (ba.py:397-403)
+__global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const int32_t* inc_con,
+                             const int32_t* inc_row, const double* e_terms, const double* cinv0,
+                             double* inc_block, double* uinc) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        for (int32_t k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+            const int32_t code = inc_con[k];
+            const int32_t e = code >> 1;
+            const double sgn = (code & 1) ? -1.0 : 1.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) acc[a] += sgn * e_terms[(int64_t)a * E + e];
+        }
+        const double c = cinv0[inc_row[i]];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            inc_block[i * 6 + a] = acc[a];
+            uinc[i * 6 + a] = acc[a] * c;
+        }
+    }
+}
+
+// pose blocks (ba.py:389-394) and Schur blocks E C0^-1 E^T (ba.py:405-413):
+// one warp per union key, fixed lane-strided order + xor-tree reduction
+__global__ void __launch_bounds__(128) k_key_blocks(
+    int64_t W, const int32_t* key_seg_ptr, const int32_t* key_seg, const double* seg_h,
+    const int64_t* key_pair_ptr, const int32_t* pair_l, const int32_t* pair_r,
+    const double* uinc, const double* inc_block, double* pose_blocks, double* schur_blocks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = warp; w < W; w += nwarps) {
+        double h[21];
+#pragma unroll
+        for (int k = 0; k < 21; ++k) h[k] = 0.0;
+        for (int32_t k = key_seg_ptr[w] + lane; k < key_seg_ptr[w + 1]; k += 32) {
+            const int32_t code = key_seg[k];
+            const double sgn = (code & 1) ? -1.0 : 1.0;
+            const double* src = seg_h + (int64_t)(code >> 1) * 21;
+#pragma unroll
+            for (int q = 0; q < 21; ++q) h[q] += sgn * src[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 21; ++q) h[q] = warp_sum(h[q]);
+        // lane j writes entries j and j+32 of the symmetric 6x6
+        for (int idx = lane; idx < 36; idx += 32) {
+            const int a = idx / 6, b = idx % 6;
+            const int t = a <= b ? utri(a, b) : utri(b, a);
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 21; ++q) v = (q == t) ? h[q] : v;
+            pose_blocks[w * 36 + idx] = v;
+        }
+        double s[36];
+#pragma unroll
+        for (int k = 0; k < 36; ++k) s[k] = 0.0;
+        for (int64_t k = key_pair_ptr[w] + lane; k < key_pair_ptr[w + 1]; k += 32) {
+            const double* u = uinc + (int64_t)pair_l[k] * 6;
+            const double* v = inc_block + (int64_t)pair_r[k] * 6;
+            double uu[6], vv[6];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) { uu[a] = u[a]; vv[a] = v[a]; }
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+#pragma unroll
+                for (int b = 0; b < 6; ++b) s[a * 6 + b] += uu[a] * vv[b];
+        }
+#pragma unroll
+        for (int k = 0; k < 36; ++k) s[k] = warp_sum(s[k]);
+        for (int idx = lane; idx < 36; idx += 32) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 36; ++q) v = (q == idx) ? s[q] : v;
+            schur_blocks[w * 36 + idx] = v;
+        }
+    }
+}
+
+// rhs_pose (ba.py:375-380) and rhs_schur = E C0^-1 w (ba.py:415-417): warp per var
+__global__ void k_var_rhs(int64_t n, const int32_t* var_seg_ptr, const int32_t* var_seg,
+                          const double* seg_g, const int32_t* var_inc_ptr, const int32_t* inc_row,
+                          const double* uinc, const double* rhs_depth, double* rhs_pose,
+                          double* rhs_schur, unsigned long long* grad_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = warp; v < n; v += nwarps) {
+        double g[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};
+        for (int32_t k = var_seg_ptr[v] + lane; k < var_seg_ptr[v + 1]; k += 32) {
+            const int32_t code = var_seg[k];
+            const double sgn = (code & 1) ? -1.0 : 1.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) g[a] += sgn * seg_g[(int64_t)(code >> 1) * 6 + a];
+        }
+        for (int32_t i = var_inc_ptr[v] + lane; i < var_inc_ptr[v + 1]; i += 32) {
+            const double r = rhs_depth[inc_row[i]];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) sc[a] += uinc[(int64_t)i * 6 + a] * r;
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            g[a] = warp_sum(g[a]);
+            sc[a] = warp_sum(sc[a]);
+        }
+        if (lane < 6) {
+            double gv = 0.0, sv = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                gv = (lane == a) ? g[a] : gv;
+                sv = (lane == a) ? sc[a] : sv;
+            }
+            rhs_pose[v * 6 + lane] = gv;
+            rhs_schur[v * 6 + lane] = sv;
+            atomicMax(grad_bits, (unsigned long long)__double_as_longlong(fabs(gv)));
+        }
+    }
+}
+
+// scale pin direction (ba.py:419-426)
+__global__ void k_pin(const double* t, int32_t first_free, int32_t anchor, double* scal) {
+    double u[3];
+    for (int k = 0; k < 3; ++k) u[k] = t[3 * first_free + k] - (anchor >= 0 ? t[3 * anchor + k] : 0.0);
+    const double nrm = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    if (nrm > 1e-9) {
+        scal[1] = 1.0;
+        for (int k = 0; k < 3; ++k) scal[2 + k] = u[k] / nrm;
+    } else {
+        scal[1] = 0.0;
+    }
+}
+
+}  // namespace
+
+int32_t objective(dpv_problem* p, const double* q, const double* t, const double* d, double* out,
+                  cudaStream_t st) {
+    DPV_TRY(frame_rotations(p, q, st));
+    k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
+                                            p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d,
+                                            p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+                                            p->obj_part);
+    DPV_CHECK_LAUNCH();
+    k_sum_parts<<<1, 1024, 0, st>>>(kObjBlocks, p->obj_part, out);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t residuals(dpv_problem* p, const double* q, const double* t, const double* d, double* res,
+                  uint8_t* valid, cudaStream_t st) {
+    DPV_TRY(frame_rotations(p, q, st));
+    if (p->E == 0) return DPV_OK;
+    k_residuals<<<grid_for(p->E, 256), 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst,
+                                                      p->a_row, p->a_pidx, p->a_tgt, p->r_ray,
+                                                      p->frame_R, t, d, p->intr[0], p->intr[1],
+                                                      p->intr[2], p->intr[3], res, valid);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
+                 cudaStream_t st) {
+    DPV_TRY(frame_rotations(p, q, st));
+    DPV_CUDA(cudaMemsetAsync(p->scal, 0, sizeof(double) * 8, st));
+    auto* grad_bits = reinterpret_cast<unsigned long long*>(p->scal);
+    auto* n_inactive = reinterpret_cast<unsigned long long*>(p->scal + 6);
+    if (p->S > 0) {
+        const int warps_per_block = 4;
+        int blocks = (int)std::min<int64_t>((p->S + warps_per_block - 1) / warps_per_block,
+                                            (int64_t)sm_count() * 64);
+        k_assemble_edges<<<blocks, 32 * warps_per_block, 0, st>>>(
+            p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,
+            p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+            p->e_terms, p->seg_h, p->seg_g);
+        DPV_CHECK_LAUNCH();
+    }
+    if (p->P > 0) {
+        k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,
+                                                     p->e_terms, p->depth_diag, p->rhs_depth,
+                                                     p->active, p->cinv0, grad_bits, n_inactive);
+        DPV_CHECK_LAUNCH();
+    }
+    if (p->I > 0) {
+        k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
+                                                           p->inc_row, p->e_terms, p->cinv0,
+                                                           p->inc_block, p->uinc);
+        DPV_CHECK_LAUNCH();
+    }
+    if (p->W > 0) {
+        int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
+        k_key_blocks<<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
+                                             p->key_pair_ptr, p->pair_l, p->pair_r, p->uinc,
+                                             p->inc_block, p->pose_blocks, p->schur_blocks);
+        DPV_CHECK_LAUNCH();
+    }
+    if (p->n > 0) {
+        int blocks = (int)std::min<int64_t>((p->n + 3) / 4, (int64_t)sm_count() * 64);
+        k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
+                                          p->var_inc_ptr, p->inc_row, p->uinc, p->rhs_depth,
+                                          p->rhs_pose, p->rhs_schur, grad_bits);
+        DPV_CHECK_LAUNCH();
+        if (p->scale_degenerate) {
+            k_pin<<<1, 1, 0, st>>>(t, p->first, p->touched0, p->scal);
+            DPV_CHECK_LAUNCH();
+        }
+    }
+    return DPV_OK;
+}
+
+}  // namespace dpv

@@ -1,0 +1,582 @@
+// extern "C" boundary (include/dpvslam_b200.h) and the native LM driver
+// restating ba.solve (ba.py:534-605).
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <unordered_set>
+#include <vector>
+
+#include "problem.cuh"
+
+namespace dpv {
+
+static thread_local std::string t_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_error = msg; }
+void clear_error() { t_error.clear(); }
+
+int sm_count() {
+    static int cached = 0;
+    if (cached == 0) {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            cached = v;
+        else
+            cached = 148;
+    }
+    return cached;
+}
+
+int32_t quat_to_matrix(const double* q, int64_t n, double* r, cudaStream_t st);
+int32_t reproject_grid(const double* rays, const double* inv_depth, const double* rot_i,
+                       const double* t_i, const double* rot_j, const double* t_j,
+                       const double* intr, int64_t E, int m, double* pix, uint8_t* valid,
+                       double* j_pose, double* j_depth, cudaStream_t st);
+int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const double* coords,
+             const int32_t* ii, const int32_t* jj, int64_t E, int C, int h0, int w0, int h1,
+             int w1, int levels, int radius, int dtype, float* out, cudaStream_t st);
+int32_t avg_pool4(const void* in, int64_t F, int H, int W, int C, int dtype, void* out,
+                  cudaStream_t st);
+
+namespace {
+
+__global__ void k_row_flags(int64_t E, const int32_t* p_row, const double* cmax, double gate,
+                            uint8_t* flag) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x)
+        if (cmax[e] > gate) flag[p_row[e]] = 1;
+}
+
+__global__ void k_count_flags(int64_t n, const uint8_t* flag, unsigned long long* out) {
+    __shared__ unsigned long long sh[32];
+    unsigned long long c = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += flag[i];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        *out = t;
+    }
+}
+
+__global__ void k_gather_depths(int64_t P, const int32_t* depth_patch, const double* all,
+                                double* d) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
+         r += (int64_t)gridDim.x * blockDim.x)
+        d[r] = all[depth_patch[r]];
+}
+
+__global__ void k_scatter_depths(int64_t P, const int32_t* depth_patch, const double* d,
+                                 double* all) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
+         r += (int64_t)gridDim.x * blockDim.x)
+        all[depth_patch[r]] = d[r];
+}
+
+// fixed-order sum of squares of two vectors -> out[0]
+__global__ void k_step_norm(int64_t n1, const double* a, int64_t n2, const double* b,
+                            double* out) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) s += a[i] * a[i];
+    double s2 = 0.0;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) s2 += b[i] * b[i];
+    s = warp_sum(s);
+    s2 = warp_sum(s2);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double tot = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sh[w];
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t2 += sh[w];
+        out[0] = sqrt(tot + t2);
+    }
+}
+
+struct ArrayDesc {
+    void* ptr;
+    int64_t count;
+    int32_t dtype;
+};
+
+bool lookup(const dpv_problem* p, const char* name, ArrayDesc& a) {
+    struct Entry {
+        const char* n;
+        const void* ptr;
+        int64_t count;
+        int32_t dtype;
+    };
+    const int64_t N = 6 * p->n;
+    const Entry table[] = {
+        {"edge_idx", p->edge_idx, p->E, 2},
+        {"p_row", p->p_row, p->E, 1},
+        {"p_pos", p->p_pos, p->E, 1},
+        {"p_vi", p->p_vi, p->E, 1},
+        {"p_vj", p->p_vj, p->E, 1},
+        {"a_src", p->a_src, p->E, 1},
+        {"a_dst", p->a_dst, p->E, 1},
+        {"a_row", p->a_row, p->E, 1},
+        {"a_pidx", p->a_pidx, p->E, 1},
+        {"a_tgt", p->a_tgt, p->E * 2 * p->m, 0},
+        {"a_w", p->a_w, p->E * 2, 0},
+        {"depth_patch", p->depth_patch, p->P, 1},
+        {"r_ray", p->r_ray, p->P * 2 * p->m, 0},
+        {"row_ptr", p->row_ptr, p->P + 1, 1},
+        {"row_pos", p->row_pos, p->E, 1},
+        {"seg_ptr", p->seg_ptr, p->S + 1, 1},
+        {"seg_src", p->seg_src, p->S, 1},
+        {"seg_dst", p->seg_dst, p->S, 1},
+        {"inc_var", p->inc_var, p->I, 1},
+        {"inc_row", p->inc_row, p->I, 1},
+        {"inc_ptr", p->inc_ptr, p->I + 1, 1},
+        {"inc_con", p->inc_con, p->NC, 1},
+        {"inc_inv", p->p_inc_inv, p->NC, 1},
+        {"var_inc_ptr", p->var_inc_ptr, p->n + 1, 1},
+        {"rinc_ptr", p->rinc_ptr, p->P + 1, 1},
+        {"rinc", p->rinc, p->I, 1},
+        {"union_keys", p->union_keys, p->W, 2},
+        {"key_pair_ptr", p->key_pair_ptr, p->W + 1, 2},
+        {"pair_l", p->pair_l, p->NP, 1},
+        {"pair_r", p->pair_r, p->NP, 1},
+        {"key_seg_ptr", p->key_seg_ptr, p->W + 1, 1},
+        {"key_seg", p->key_seg, p->KS, 1},
+        {"var_seg_ptr", p->var_seg_ptr, p->n + 1, 1},
+        {"var_seg", p->var_seg, p->VS, 1},
+        {"key_a", p->key_a, p->W, 1},
+        {"key_b", p->key_b, p->W, 1},
+        {"touched", p->touched, p->T, 1},
+        {"e_terms", p->e_terms, p->E * 8, 0},
+        {"seg_h", p->seg_h, p->S * 21, 0},
+        {"seg_g", p->seg_g, p->S * 6, 0},
+        {"depth_diag", p->depth_diag, p->P, 0},
+        {"rhs_depth", p->rhs_depth, p->P, 0},
+        {"active", p->active, p->P, 3},
+        {"cinv0", p->cinv0, p->P, 0},
+        {"inc_block", p->inc_block, p->I * 6, 0},
+        {"pose_blocks", p->pose_blocks, p->W * 36, 0},
+        {"schur_blocks", p->schur_blocks, p->W * 36, 0},
+        {"rhs_pose", p->rhs_pose, p->n * 6, 0},
+        {"rhs_schur", p->rhs_schur, p->n * 6, 0},
+        {"scal", p->scal, 16, 0},
+        {"dense", p->dense, p->dense ? (N + 1) * p->dense_ld : 0, 0},
+    };
+    for (const Entry& e : table) {
+        if (std::strcmp(e.n, name) == 0) {
+            a.ptr = const_cast<void*>(e.ptr);
+            a.count = e.count;
+            a.dtype = e.dtype;
+            return true;
+        }
+    }
+    return false;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+}  // namespace
+}  // namespace dpv
+
+using namespace dpv;
+
+extern "C" {
+
+int32_t dpv_abi_version(void) { return DPV_ABI_VERSION; }
+
+const char* dpv_last_error(void) { return t_error.c_str(); }
+
+int64_t dpv_launch_count(void) { return g_launches.load(); }
+
+int32_t dpv_device_info(int32_t* sms, int32_t* major, int32_t* minor) {
+    int dev = 0;
+    DPV_CUDA(cudaGetDevice(&dev));
+    int v = 0;
+    DPV_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    if (sms) *sms = v;
+    DPV_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major) *major = v;
+    DPV_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev));
+    if (minor) *minor = v;
+    return DPV_OK;
+}
+
+int32_t dpv_quat_to_matrix(const double* q, int64_t n, double* rot, void* stream) {
+    clear_error();
+    DPV_ARG(n >= 0 && (n == 0 || (q && rot)), "bad quat_to_matrix args");
+    return quat_to_matrix(q, n, rot, as_stream(stream));
+}
+
+int32_t dpv_reproject_grid(const double* rays, const double* inv_depth, const double* rot_i,
+                           const double* t_i, const double* rot_j, const double* t_j,
+                           const double* intr4, int64_t n_edges, int32_t cells, double* pix,
+                           uint8_t* valid, double* j_pose, double* j_depth, void* stream) {
+    clear_error();
+    DPV_ARG(n_edges >= 0 && cells > 0 && intr4, "bad reproject_grid args");
+    return reproject_grid(rays, inv_depth, rot_i, t_i, rot_j, t_j, intr4, n_edges, cells, pix,
+                          valid, j_pose, j_depth, as_stream(stream));
+}
+
+int32_t dpv_problem_create(const dpv_graph* graph, int32_t first_free, int32_t last_free,
+                           const int64_t* edge_indices, int64_t n_edge_indices, void* stream,
+                           dpv_problem** out) {
+    clear_error();
+    DPV_ARG(out != nullptr, "out is NULL");
+    *out = nullptr;
+    dpv_problem* p = new (std::nothrow) dpv_problem();
+    DPV_ARG(p != nullptr, "allocation failed");
+    int32_t s = build_problem(graph, first_free, last_free, edge_indices, n_edge_indices,
+                              as_stream(stream), p);
+    if (s != DPV_OK) {
+        delete p;
+        return s;
+    }
+    *out = p;
+    return DPV_OK;
+}
+
+int32_t dpv_problem_destroy(dpv_problem* prob) {
+    delete prob;
+    return DPV_OK;
+}
+
+int32_t dpv_problem_get_info(const dpv_problem* p, dpv_problem_info* info) {
+    DPV_ARG(p && info, "NULL argument");
+    info->n_edges = p->E;
+    info->n_depths = p->P;
+    info->n_free = p->n;
+    info->n_keys = p->W;
+    info->n_inc = p->I;
+    info->n_pairs = p->NP;
+    info->n_segments = p->S;
+    info->n_touched = p->T;
+    info->first_free = p->first;
+    info->last_free = p->last;
+    info->scale_degenerate = p->scale_degenerate;
+    info->touched_fixed0 = p->touched0;
+    info->device_bytes = p->bytes;
+    return DPV_OK;
+}
+
+int32_t dpv_problem_array(const dpv_problem* p, const char* name, void** ptr, int64_t* count,
+                          int32_t* dtype) {
+    clear_error();
+    DPV_ARG(p && name && ptr && count && dtype, "NULL argument");
+    ArrayDesc a;
+    if (!lookup(p, name, a)) {
+        set_error(std::string("unknown array ") + name);
+        return DPV_BAD_ARGS;
+    }
+    *ptr = a.ptr;
+    *count = a.count;
+    *dtype = a.dtype;
+    return DPV_OK;
+}
+
+int32_t dpv_gather_depths(const dpv_problem* p, const double* patch_depth, double* d,
+                          void* stream) {
+    clear_error();
+    DPV_ARG(p, "NULL problem");
+    if (p->P == 0) return DPV_OK;
+    k_gather_depths<<<grid_for(p->P, 256), 256, 0, as_stream(stream)>>>(p->P, p->depth_patch,
+                                                                        patch_depth, d);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t dpv_scatter_depths(const dpv_problem* p, const double* d, double* patch_depth,
+                           void* stream) {
+    clear_error();
+    DPV_ARG(p, "NULL problem");
+    if (p->P == 0) return DPV_OK;
+    k_scatter_depths<<<grid_for(p->P, 256), 256, 0, as_stream(stream)>>>(p->P, p->depth_patch,
+                                                                         d, patch_depth);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t dpv_active_patch_count(dpv_problem* p, double gate, int64_t* count, void* stream) {
+    clear_error();
+    DPV_ARG(p && count, "NULL argument");
+    cudaStream_t st = as_stream(stream);
+    *count = 0;
+    if (p->P == 0) return DPV_OK;
+    DPV_CUDA(cudaMemsetAsync(p->row_flag, 0, p->P, st));
+    k_row_flags<<<grid_for(p->E, 256), 256, 0, st>>>(p->E, p->p_row, p->p_conf_max, gate,
+                                                     p->row_flag);
+    DPV_CHECK_LAUNCH();
+    auto* out = reinterpret_cast<unsigned long long*>(p->count_buf);
+    k_count_flags<<<1, 1024, 0, st>>>(p->P, p->row_flag, out);
+    DPV_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    DPV_CUDA(cudaMemcpyAsync(&h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DPV_CUDA(cudaStreamSynchronize(st));
+    *count = (int64_t)h;
+    return DPV_OK;
+}
+
+int32_t dpv_residuals(dpv_problem* p, const double* q, const double* t, const double* d,
+                      double* res, uint8_t* valid, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && (d || p->P == 0) && (res || p->E == 0), "NULL argument");
+    return residuals(p, q, t, d, res, valid, as_stream(stream));
+}
+
+int32_t dpv_objective(dpv_problem* p, const double* q, const double* t, const double* d,
+                      double* out_dev, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && out_dev, "NULL argument");
+    return objective(p, q, t, d, out_dev, as_stream(stream));
+}
+
+int32_t dpv_assemble(dpv_problem* p, const double* q, const double* t, const double* d,
+                     void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t, "NULL argument");
+    return assemble(p, q, t, d, as_stream(stream));
+}
+
+int32_t dpv_reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
+                           void* stream) {
+    clear_error();
+    DPV_ARG(p, "NULL problem");
+    return reduced_system(p, lam, blocks, rhs, cinv, as_stream(stream));
+}
+
+int32_t dpv_solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status_dev,
+                  void* stream) {
+    clear_error();
+    DPV_ARG(p && dp && (dd || p->P == 0) && status_dev, "NULL argument");
+    return solve(p, lam, dp, dd, status_dev, as_stream(stream));
+}
+
+int32_t dpv_back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
+                            void* stream) {
+    clear_error();
+    DPV_ARG(p && dp && (dd || p->P == 0), "NULL argument");
+    return back_substitute(p, lam, dp, dd, as_stream(stream));
+}
+
+int32_t dpv_apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
+                       const double* dp, const double* dd, double* q2, double* t2, double* d2,
+                       void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && dp && q2 && t2, "NULL argument");
+    return apply_step(p, q, t, d, dp, dd, q2, t2, d2, as_stream(stream));
+}
+
+int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
+                     const dpv_lm_params* params, dpv_lm_report* rep, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && params && rep, "NULL argument");
+    cudaStream_t st = as_stream(stream);
+    const double kGrow = 10.0, kShrink = 0.5, kMax = 1e10;  // ba.py:40-44
+    const int kEscalations = 12;
+    std::memset(rep, 0, sizeof(*rep));
+    const int64_t F = p->F, P = p->P;
+    double* wq = p->lm_wq;
+    double* wt = p->lm_wt;
+    double* wd = p->lm_wd;
+    DPV_CUDA(cudaMemcpyAsync(wq, q, sizeof(double) * F * 4, cudaMemcpyDeviceToDevice, st));
+    DPV_CUDA(cudaMemcpyAsync(wt, t, sizeof(double) * F * 3, cudaMemcpyDeviceToDevice, st));
+    if (P) DPV_CUDA(cudaMemcpyAsync(wd, d, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
+    double* h = p->lm_host;  // pinned: [0] obj, [1] status, [2] step norm, [3] grad, [4] inact
+    double* dev_scalar = p->scal + 8;  // scal[8..15] LM scalars on the device
+    DPV_TRY(objective(p, wq, wt, wd, dev_scalar, st));
+    DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    DPV_CUDA(cudaStreamSynchronize(st));
+    double obj = h[0];
+    rep->initial_objective = obj;
+    rep->final_objective = obj;
+    rep->gradient_norm = INFINITY;
+    rep->step_norm = INFINITY;
+    double lam = params->lambda0;
+    int32_t* status = p->status;
+    for (int it = 0; it < params->max_iterations; ++it) {
+        const double tic = now_s();
+        DPV_TRY(assemble(p, wq, wt, wd, st));
+        DPV_CUDA(cudaMemcpyAsync(h + 3, p->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+        DPV_CUDA(cudaMemcpyAsync(h + 4, p->scal + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
+        bool accepted = false, solved_once = false, singular = false;
+        double grad = 0.0;
+        int64_t inactive = 0;
+        bool grad_read = false;
+        for (int att = 0; att <= kEscalations; ++att) {
+            rep->n_attempts++;
+            DPV_TRY(solve(p, lam, p->lm_dp, p->lm_dd, status, st));
+            DPV_TRY(apply_step(p, wq, wt, wd, p->lm_dp, p->lm_dd, p->lm_q, p->lm_t, p->lm_d, st));
+            DPV_TRY(objective(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
+            k_step_norm<<<1, 256, 0, st>>>(6 * p->n, p->lm_dp, P, p->lm_dd, dev_scalar + 1);
+            DPV_CHECK_LAUNCH();
+            DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+            DPV_CUDA(cudaMemcpyAsync(h + 2, dev_scalar + 1, sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+            int32_t sflag = 0;
+            DPV_CUDA(cudaMemcpyAsync(&sflag, status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            DPV_CUDA(cudaStreamSynchronize(st));
+            if (!grad_read) {
+                unsigned long long gb;
+                std::memcpy(&gb, h + 3, sizeof(gb));
+                std::memcpy(&grad, &gb, sizeof(grad));
+                unsigned long long ib;
+                std::memcpy(&ib, h + 4, sizeof(ib));
+                inactive = (int64_t)ib;
+                rep->gradient_norm = grad;
+                rep->unconstrained_depths = inactive;
+                grad_read = true;
+            }
+            if (sflag != 0) {  // SingularSystem from the factorisation (ba.py:566-571)
+                singular = true;
+                lam *= kGrow;
+                if (lam > kMax) {
+                    set_error("dense factorization failed: matrix not positive definite");
+                    return DPV_SINGULAR;
+                }
+                continue;
+            }
+            solved_once = true;
+            const double cand = h[0];
+            if (cand <= obj * (1 + 1e-12) + 1e-300) {  // ba.py:575
+                std::swap(wq, p->lm_q);
+                std::swap(wt, p->lm_t);
+                std::swap(wd, p->lm_d);
+                obj = cand < obj ? cand : obj;
+                rep->step_norm = h[2];
+                lam = lam * kShrink > 1e-12 ? lam * kShrink : 1e-12;
+                accepted = true;
+                break;
+            }
+            lam *= kGrow;
+            if (lam > kMax) break;
+        }
+        if (rep->times_len < 64) rep->iteration_times[rep->times_len++] = now_s() - tic;
+        if (!accepted) {
+            if (singular && !solved_once) {
+                set_error("dense factorization failed: matrix not positive definite");
+                return DPV_SINGULAR;
+            }
+            break;
+        }
+        rep->iterations++;
+        rep->final_objective = obj;
+        if (grad < params->tolerance) {
+            rep->converged = 1;
+            break;
+        }
+    }
+    if (rep->gradient_norm < params->tolerance) rep->converged = 1;
+    rep->final_damping = lam;
+    // write the accepted state back (ba.py:604)
+    DPV_CUDA(cudaMemcpyAsync(q, wq, sizeof(double) * F * 4, cudaMemcpyDeviceToDevice, st));
+    DPV_CUDA(cudaMemcpyAsync(t, wt, sizeof(double) * F * 3, cudaMemcpyDeviceToDevice, st));
+    if (P) DPV_CUDA(cudaMemcpyAsync(d, wd, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
+    // keep the handle's buffer ownership consistent after swaps
+    p->lm_wq = wq;
+    p->lm_wt = wt;
+    p->lm_wd = wd;
+    DPV_CUDA(cudaStreamSynchronize(st));
+    return DPV_OK;
+}
+
+int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev, void* stream) {
+    clear_error();
+    DPV_ARG(a && b && status_dev && n > 0, "bad cholesky_solve args");
+    cudaStream_t st = as_stream(stream);
+    // augmented copy: rows 0..n-1 = a, row n = b
+    const int64_t ld = ((n + 1 + 7) / 8) * 8;
+    double* aug = nullptr;
+    double* work = nullptr;
+    DPV_CUDA(cudaMallocAsync(&aug, sizeof(double) * (n + 1) * ld, st));
+    DPV_CUDA(cudaMallocAsync(&work, sizeof(double) * cholesky_work_doubles(n), st));
+    DPV_CUDA(cudaMemsetAsync(aug, 0, sizeof(double) * (n + 1) * ld, st));
+    DPV_CUDA(cudaMemcpy2DAsync(aug, ld * sizeof(double), a, n * sizeof(double), n * sizeof(double),
+                               n, cudaMemcpyDeviceToDevice, st));
+    DPV_CUDA(cudaMemcpyAsync(aug + n * ld, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    int32_t s = cholesky_solve(aug, ld, b, n, status_dev, work, st);
+    if (s == DPV_OK) {
+        DPV_CUDA(cudaMemcpy2DAsync(a, n * sizeof(double), aug, ld * sizeof(double),
+                                   n * sizeof(double), n, cudaMemcpyDeviceToDevice, st));
+    }
+    cudaFreeAsync(aug, st);
+    cudaFreeAsync(work, st);
+    return s;
+}
+
+int32_t dpv_block_fill_count(const int64_t* keys, int64_t n_keys, int64_t n, int64_t* count) {
+    // symbolic restatement of block_cholesky.py:54-105 (fill only, no numerics)
+    clear_error();
+    DPV_ARG(count && n >= 0 && (n_keys == 0 || keys), "bad block_fill_count args");
+    std::vector<std::set<int64_t>> below(n);
+    std::vector<char> diag(n, 0);
+    std::unordered_set<uint64_t> lower;
+    lower.reserve((size_t)n_keys * 2 + 16);
+    auto code = [n](int64_t i, int64_t k) { return (uint64_t)i * (uint64_t)n + (uint64_t)k; };
+    for (int64_t w = 0; w < n_keys; ++w) {
+        const int64_t a = keys[2 * w], b = keys[2 * w + 1];
+        DPV_ARG(0 <= a && a <= b && b < n, "block keys must satisfy 0 <= a <= b < n");
+        if (a == b) {
+            diag[a] = 1;
+        } else {
+            lower.insert(code(b, a));
+            below[a].insert(b);
+        }
+    }
+    int64_t total = n;
+    for (int64_t j = 0; j < n; ++j) {
+        if (!diag[j]) {
+            set_error("missing diagonal block " + std::to_string(j));
+            return DPV_SINGULAR;
+        }
+        const std::vector<int64_t> rows(below[j].begin(), below[j].end());
+        total += (int64_t)rows.size();
+        for (size_t pi = 0; pi < rows.size(); ++pi) {
+            const int64_t i = rows[pi];
+            for (size_t qi = 0; qi <= pi; ++qi) {
+                const int64_t k = rows[qi];
+                if (i == k) {
+                    diag[i] = 1;
+                } else if (lower.insert(code(i, k)).second) {
+                    below[k].insert(i);
+                }
+            }
+        }
+    }
+    *count = total;
+    return DPV_OK;
+}
+
+int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1, const double* coords,
+                 const int32_t* ii, const int32_t* jj, int64_t n_edges, int32_t channels,
+                 int32_t h0, int32_t w0, int32_t h1, int32_t w1, int32_t n_levels,
+                 int32_t radius, int32_t dtype, float* out, void* stream) {
+    clear_error();
+    DPV_ARG(n_edges >= 0 && channels > 0 && (n_levels == 1 || n_levels == 2) && radius >= 0 &&
+                radius <= 4 && (dtype == 0 || dtype == 1),
+            "bad corr args");
+    DPV_ARG(n_edges == 0 || (gmap && fmap0 && coords && ii && jj && out), "NULL corr argument");
+    DPV_ARG(n_levels == 1 || fmap1, "level-1 feature map missing");
+    return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,
+                radius, dtype, out, as_stream(stream));
+}
+
+int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
+                      int32_t dtype, void* out, void* stream) {
+    clear_error();
+    DPV_ARG(fmap && out && n_frames >= 0 && h > 0 && w > 0 && channels > 0 &&
+                (dtype == 0 || dtype == 1),
+            "bad avg_pool4 args");
+    return avg_pool4(fmap, n_frames, h, w, channels, dtype, out, as_stream(stream));
+}
+
+}  // extern "C"

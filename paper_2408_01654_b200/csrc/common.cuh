@@ -1,0 +1,120 @@
+// Shared helpers for the sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/dpvslam_b200.h"
+
+namespace dpv {
+
+// ---------------------------------------------------------------------------
+// error plumbing: never throw across the C ABI
+
+void set_error(const std::string& msg);
+void clear_error();
+extern std::atomic<int64_t> g_launches;
+
+struct Status {
+    int32_t code = DPV_OK;
+    bool ok() const { return code == DPV_OK; }
+};
+
+#define DPV_CUDA(expr)                                                              \
+    do {                                                                            \
+        cudaError_t _e = (expr);                                                    \
+        if (_e != cudaSuccess) {                                                    \
+            ::dpv::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) +   \
+                             " @ " + __FILE__ + ":" + std::to_string(__LINE__));    \
+            return DPV_CUDA_ERROR;                                                  \
+        }                                                                           \
+    } while (0)
+
+#define DPV_CHECK_LAUNCH()                                                          \
+    do {                                                                            \
+        ::dpv::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
+        cudaError_t _e = cudaGetLastError();                                        \
+        if (_e != cudaSuccess) {                                                    \
+            ::dpv::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e) + \
+                             " @ " + __FILE__ + ":" + std::to_string(__LINE__));    \
+            return DPV_CUDA_ERROR;                                                  \
+        }                                                                           \
+    } while (0)
+
+#define DPV_TRY(expr)                                                               \
+    do {                                                                            \
+        int32_t _s = (expr);                                                        \
+        if (_s != DPV_OK) return _s;                                                \
+    } while (0)
+
+#define DPV_ARG(cond, msg)                                                          \
+    do {                                                                            \
+        if (!(cond)) {                                                              \
+            ::dpv::set_error(msg);                                                  \
+            return DPV_BAD_ARGS;                                                    \
+        }                                                                           \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int block, int cap = 148 * 32) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<int>(g);
+}
+
+int sm_count();
+
+// raise a kernel's dynamic shared-memory limit to `bytes` (once per growth)
+template <typename K>
+int32_t ensure_smem(K kernel, size_t bytes, size_t& current) {
+    if (bytes > current) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)bytes);
+        if (e != cudaSuccess) {
+            set_error(std::string("cudaFuncSetAttribute(smem ") + std::to_string(bytes) +
+                      "): " + cudaGetErrorString(e));
+            return DPV_CUDA_ERROR;
+        }
+        current = bytes;
+    }
+    return DPV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device math
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// quaternion (x,y,z,w) -> row-major rotation; restates geometry.py:70-86
+__device__ __forceinline__ void quat_to_rot(const double* q, double* r) {
+    const double x = q[0], y = q[1], z = q[2], w = q[3];
+    const double xx = x * x, yy = y * y, zz = z * z;
+    const double xy = x * y, xz = x * z, yz = y * z;
+    const double wx = w * x, wy = w * y, wz = w * z;
+    r[0] = 1.0 - 2.0 * (yy + zz);
+    r[1] = 2.0 * (xy - wz);
+    r[2] = 2.0 * (xz + wy);
+    r[3] = 2.0 * (xy + wz);
+    r[4] = 1.0 - 2.0 * (xx + zz);
+    r[5] = 2.0 * (yz - wx);
+    r[6] = 2.0 * (xz - wy);
+    r[7] = 2.0 * (yz + wx);
+    r[8] = 1.0 - 2.0 * (xx + yy);
+}
+
+constexpr double kDepthEps = 1e-8;          // geometry.py:24
+constexpr double kInverseDepthFloor = 1e-6; // geometry.py:28
+constexpr double kSmallAngle = 1e-8;        // geometry.py:26
+constexpr double kActiveEps = 1e-12;        // ba.py:47
+
+}  // namespace dpv

@@ -1,0 +1,162 @@
+// Device-resident BA problem: state-independent index (ba.py:60-216) and the
+// assembled system arrays (ba.py:272-440).  One handle per BAProblem.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct dpv_problem {
+    // ---- sizes -------------------------------------------------------------
+    int32_t F = 0;      // graph frames
+    int32_t m = 9;      // cells per patch
+    int64_t E = 0;      // problem edges
+    int64_t P = 0;      // depth rows
+    int64_t n = 0;      // free poses
+    int64_t W = 0;      // union keys
+    int64_t I = 0;      // incidences
+    int64_t NP = 0;     // Schur pairs
+    int64_t S = 0;      // edge segments
+    int64_t NC = 0;     // incidence contributions
+    int64_t T = 0;      // touched fixed frames
+    int64_t KS = 0;     // key->segment entries
+    int64_t VS = 0;     // var->segment entries
+    int32_t first = 0, last = 0;
+    int32_t scale_degenerate = 0;
+    int32_t touched0 = -1;
+    double intr[4] = {0, 0, 0, 0};
+
+    // ---- problem-order arrays ---------------------------------------------
+    int64_t* edge_idx = nullptr;   // (E) graph edge index
+    int32_t* p_row = nullptr;      // (E) depth row
+    int32_t* p_pos = nullptr;      // (E) assembly position
+    int32_t* p_vi = nullptr;       // (E) var of src or -1
+    int32_t* p_vj = nullptr;       // (E) var of dst or -1
+    double* p_conf_max = nullptr;  // (E) max confidence (active_patch_count)
+
+    // ---- assembly-order (segment-sorted) SoA arrays -----------------------
+    int32_t* a_src = nullptr;      // (E)
+    int32_t* a_dst = nullptr;      // (E)
+    int32_t* a_row = nullptr;      // (E)
+    int32_t* a_pidx = nullptr;     // (E) problem index
+    double* a_tgt = nullptr;       // (2m, E)
+    double* a_w = nullptr;         // (2, E)
+
+    // ---- depth rows ---------------------------------------------------------
+    int32_t* depth_patch = nullptr;  // (P) global patch id, sorted
+    double* r_ray = nullptr;         // (2m, P) ray x,y per cell (z = 1)
+    int32_t* row_ptr = nullptr;      // (P+1) CSR over assembly positions
+    int32_t* row_pos = nullptr;      // (E)
+
+    // ---- segments (same (src,dst), <= kSegMax edges) ------------------------
+    int32_t* seg_ptr = nullptr;    // (S+1)
+    int32_t* seg_src = nullptr;    // (S)
+    int32_t* seg_dst = nullptr;    // (S)
+
+    // ---- incidences ---------------------------------------------------------
+    int32_t* inc_var = nullptr;    // (I)  sorted by (var, row) (np.unique order)
+    int32_t* inc_row = nullptr;    // (I)
+    int32_t* inc_ptr = nullptr;    // (I+1) CSR over contributions
+    int32_t* inc_con = nullptr;    // (NC) assembly position * 2 + (negative)
+    int32_t* p_inc_inv = nullptr;  // (NC) reference inc_inv (contribution -> incidence)
+    int32_t* var_inc_ptr = nullptr;  // (n+1) incidence range per var
+    int32_t* rinc_ptr = nullptr;   // (P+1) incidences per row (ascending var)
+    int32_t* rinc = nullptr;       // (I)
+
+    // ---- pose-pair keys -------------------------------------------------------
+    int64_t* union_keys = nullptr; // (W) a*n+b, a<=b
+    int64_t* key_pair_ptr = nullptr;  // (W+1)
+    int32_t* pair_l = nullptr;     // (NP) incidence index (left)
+    int32_t* pair_r = nullptr;     // (NP) incidence index (right)
+    int32_t* key_seg_ptr = nullptr;   // (W+1)
+    int32_t* key_seg = nullptr;    // (KS) seg*2 + (negative)
+    int32_t* var_seg_ptr = nullptr;   // (n+1)
+    int32_t* var_seg = nullptr;    // (VS) seg*2 + (negative)
+    int32_t* key_a = nullptr;      // (W) block row var
+    int32_t* key_b = nullptr;      // (W) block col var
+    int32_t* touched = nullptr;    // (T)
+
+    // ---- assembled system -----------------------------------------------------
+    double* frame_R = nullptr;     // (F, 9)
+    double* e_terms = nullptr;     // (8, E): e_pd[6], c_dd, g_d
+    double* seg_h = nullptr;       // (S, 21) upper-triangular sum of J^T W J
+    double* seg_g = nullptr;       // (S, 6)  sum of J^T W r
+    double* depth_diag = nullptr;  // (P)
+    double* rhs_depth = nullptr;   // (P)
+    uint8_t* active = nullptr;     // (P)
+    double* cinv0 = nullptr;       // (P)
+    double* inc_block = nullptr;   // (I, 6)
+    double* uinc = nullptr;        // (I, 6) inc_block * cinv0[row]
+    double* pose_blocks = nullptr; // (W, 36)
+    double* schur_blocks = nullptr;// (W, 36)
+    double* rhs_pose = nullptr;    // (n, 6)
+    double* rhs_schur = nullptr;   // (n, 6)
+    double* scal = nullptr;        // [0]=grad bits, [1]=pin flag, [2..4]=pin u, [5]=objective,
+                                   // [6]=unconstrained count, [7] spare
+    double* obj_part = nullptr;    // (kObjBlocks)
+    int64_t* count_buf = nullptr;  // (2) scratch counters
+
+    // ---- solve workspace -----------------------------------------------------
+    double* red_rhs = nullptr;     // (N)
+    double* cinv = nullptr;        // (P)
+    double* dense = nullptr;       // (N+1) x ld lower, lazily allocated
+    int64_t dense_ld = 0;
+    double* bsub_part = nullptr;   // back-substitution partials
+    int32_t* status = nullptr;     // (4) device flags
+
+    // ---- LM scratch ------------------------------------------------------------
+    double* lm_q = nullptr; double* lm_t = nullptr; double* lm_d = nullptr;
+    double* lm_dp = nullptr; double* lm_dd = nullptr;
+    double* lm_wq = nullptr; double* lm_wt = nullptr; double* lm_wd = nullptr;
+    uint8_t* row_flag = nullptr;   // (P) scratch for active_patch_count
+    double* lm_host = nullptr;     // pinned host scalars
+
+    std::vector<void*> allocs;     // everything above, freed by destroy
+    int64_t bytes = 0;
+
+    template <typename T>
+    int32_t alloc(T** p, int64_t count) {
+        size_t b = sizeof(T) * (size_t)(count > 0 ? count : 1);
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, b);
+        if (e != cudaSuccess) {
+            dpv::set_error(std::string("cudaMalloc ") + std::to_string(b) + ": " +
+                           cudaGetErrorString(e));
+            return DPV_CUDA_ERROR;
+        }
+        allocs.push_back(q);
+        bytes += (int64_t)b;
+        *p = reinterpret_cast<T*>(q);
+        return DPV_OK;
+    }
+    ~dpv_problem() {
+        for (void* p : allocs) cudaFree(p);
+        if (lm_host) cudaFreeHost(lm_host);
+    }
+};
+
+namespace dpv {
+constexpr int kSegMax = 128;      // edges per segment chunk
+constexpr int kObjBlocks = 1184;  // 148 SMs x 8
+int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int64_t* eidx,
+                      int64_t n_eidx, cudaStream_t st, dpv_problem* P);
+int32_t frame_rotations(dpv_problem* p, const double* q, cudaStream_t st);
+int32_t objective(dpv_problem* p, const double* q, const double* t, const double* d,
+                  double* out, cudaStream_t st);
+int32_t residuals(dpv_problem* p, const double* q, const double* t, const double* d,
+                  double* res, uint8_t* valid, cudaStream_t st);
+int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
+                 cudaStream_t st);
+int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
+                       cudaStream_t st);
+int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,
+              cudaStream_t st);
+int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
+                   const double* dp, const double* dd, double* q2, double* t2, double* d2,
+                   cudaStream_t st);
+int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
+                        cudaStream_t st);
+int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* status,
+                       double* work, cudaStream_t st);
+int64_t cholesky_work_doubles(int64_t n);
+}  // namespace dpv

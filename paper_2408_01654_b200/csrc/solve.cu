@@ -1,0 +1,585 @@
+// K4b-K4d: damped Schur-reduced camera system (ba.py:303-319), dense
+// Cholesky solve of S(lambda) with the trailing pose-block contraction on the
+// FP64 tensor cores (mma.sync m8n8k4 -> SASS DMMA; tcgen05 has no f64 kind),
+// back-substitution of the inverse depths (ba.py:321-325) and the
+// retraction (ba.py:521-531).
+//
+// Dense layout: (N+1) x ld row-major, lower triangle; row N carries the right
+// hand side, so the right-looking factorisation performs the forward
+// substitution y = L^-1 b for free (the augmented-matrix trick).
+#include <cooperative_groups.h>
+
+#include "problem.cuh"
+
+namespace dpv {
+namespace {
+
+constexpr int kNB = 64;           // panel width (K of the DMMA contraction)
+constexpr int kSmallMax = 162;    // n <= 27 poses: single-CTA shared-memory solve
+constexpr int kTile = 64;         // SYRK output tile
+
+// S(lam) block value at entry (i, j) of key w (ba.py:305-309)
+__device__ __forceinline__ double reduced_entry(const double* pose, const double* schur,
+                                                int64_t w, int idx, bool diag, double lam) {
+    double v = pose[w * 36 + idx] - schur[w * 36 + idx] / (1.0 + lam);
+    if (diag && (idx / 6 == idx % 6)) v += lam * pose[w * 36 + idx];
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// reduced system export (parity) -------------------------------------------
+
+__global__ void k_reduced_blocks(int64_t W, const int32_t* ka, const int32_t* kb,
+                                 const double* pose, const double* schur, double lam,
+                                 const double* scal, double* out) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < W * 36;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = x / 36;
+        const int idx = (int)(x % 36);
+        const bool diag = ka[w] == kb[w];
+        double v = reduced_entry(pose, schur, w, idx, diag, lam);
+        if (w == 0 && scal[1] != 0.0 && diag && ka[0] == 0) {
+            const int i = idx / 6, j = idx % 6;
+            if (i < 3 && j < 3) {
+                double mx = 0.0;
+                for (int k = 0; k < 6; ++k)
+                    mx = fmax(mx, fabs(reduced_entry(pose, schur, 0, k * 7, true, lam)));
+                const double mu = 1e6 * fmax(1.0, mx);
+                v += mu * scal[2 + i] * scal[2 + j];
+            }
+        }
+        out[x] = v;
+    }
+}
+
+__global__ void k_reduced_vectors(int64_t n6, int64_t P, const double* rhs_pose,
+                                  const double* rhs_schur, const double* depth_diag,
+                                  const uint8_t* active, double lam, double* rhs, double* cinv) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n6 + P;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        if (x < n6) {
+            if (rhs) rhs[x] = rhs_pose[x] - rhs_schur[x] / (1.0 + lam);
+        } else {
+            const int64_t r = x - n6;
+            if (cinv) cinv[r] = active[r] ? 1.0 / (depth_diag[r] * (1.0 + lam)) : 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dense scatter of S(lam) into the lower triangle + rhs row ---------------------
+
+__global__ void k_dense_scatter(int64_t W, const int32_t* ka, const int32_t* kb,
+                                const double* pose, const double* schur, double lam, double* A,
+                                int64_t ld) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < W * 36;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = x / 36;
+        const int idx = (int)(x % 36);
+        const int i = idx / 6, j = idx % 6;
+        const int64_t a = ka[w], b = kb[w];
+        const double v = reduced_entry(pose, schur, w, idx, a == b, lam);
+        if (a == b) {
+            if (i >= j) A[(6 * a + i) * ld + 6 * a + j] = v;
+        } else {
+            // upper block S_ab -> lower mirror S_ba = S_ab^T
+            A[(6 * b + j) * ld + 6 * a + i] = v;
+        }
+    }
+}
+
+__global__ void k_dense_pin_rhs(int64_t n6, const double* rhs_pose, const double* rhs_schur,
+                                double lam, const double* scal, double* A, int64_t ld) {
+    const int64_t N = n6;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
+         c += (int64_t)gridDim.x * blockDim.x)
+        A[N * ld + c] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && scal[1] != 0.0 && N >= 6) {
+        double mx = 0.0;
+        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[k * ld + k]));
+        const double mu = 1e6 * fmax(1.0, mx);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j <= i; ++j) A[i * ld + j] += mu * scal[2 + i] * scal[2 + j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// in-shared-memory factor of an nb x nb lower block (right-looking).  Returns
+// through *bad the first non-positive pivot (LAPACK potrf semantics).
+
+__device__ void smem_potrf(double* L, int ldl, int nb, int* bad, int pivot_base,
+                           int* status) {
+    for (int j = 0; j < nb; ++j) {
+        if (threadIdx.x == 0) {
+            double piv = L[j * ldl + j];
+            if (!(piv > 0.0)) {
+                if (*bad < 0) *bad = pivot_base + j;
+                piv = 1.0;
+            }
+            L[j * ldl + j] = sqrt(piv);
+        }
+        __syncthreads();
+        const double ljj = L[j * ldl + j];
+        for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) L[i * ldl + j] /= ljj;
+        __syncthreads();
+        const int rem = nb - j - 1;
+        for (int x = threadIdx.x; x < rem * rem; x += blockDim.x) {
+            const int i = j + 1 + x / rem, k = j + 1 + x % rem;
+            if (k <= i) L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j];
+        }
+        __syncthreads();
+    }
+    (void)status;
+}
+
+// ---------------------------------------------------------------------------
+// small systems: everything in one CTA, shared memory ---------------------------
+
+__global__ void __launch_bounds__(1024) k_small_solve(
+    int64_t n, int64_t W, const int32_t* ka, const int32_t* kb, const double* pose,
+    const double* schur, const double* rhs_pose, const double* rhs_schur, const double* scal,
+    double lam, double* dp, int32_t* status) {
+    extern __shared__ double A[];
+    __shared__ double col[kSmallMax + 1];
+    __shared__ int bad;
+    const int N = (int)(6 * n);
+    const int ld = N + 1;
+    const int tid = threadIdx.x;
+    const int nt = blockDim.x;
+    for (int x = tid; x < (N + 1) * ld; x += nt) A[x] = 0.0;
+    if (tid == 0) bad = -1;
+    __syncthreads();
+    for (int64_t x = tid; x < W * 36; x += nt) {
+        const int64_t w = x / 36;
+        const int idx = (int)(x % 36);
+        const int i = idx / 6, j = idx % 6;
+        const int a = ka[w], b = kb[w];
+        const double v = reduced_entry(pose, schur, w, idx, a == b, lam);
+        if (a == b) {
+            if (i >= j) A[(6 * a + i) * ld + 6 * a + j] = v;
+        } else {
+            A[(6 * b + j) * ld + 6 * a + i] = v;
+        }
+    }
+    for (int c = tid; c < N; c += nt) A[N * ld + c] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
+    __syncthreads();
+    if (tid == 0 && scal[1] != 0.0 && N >= 6) {
+        double mx = 0.0;
+        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[k * ld + k]));
+        const double mu = 1e6 * fmax(1.0, mx);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j <= i; ++j) A[i * ld + j] += mu * scal[2 + i] * scal[2 + j];
+    }
+    __syncthreads();
+    // right-looking Cholesky over columns 0..N-1; row N is the rhs
+    const int lane = tid & 31, wy = tid >> 5, ny = nt >> 5;
+    for (int j = 0; j < N; ++j) {
+        if (tid == 0) {
+            double piv = A[j * ld + j];
+            if (!(piv > 0.0)) {
+                if (bad < 0) bad = j;
+                piv = 1.0;
+            }
+            A[j * ld + j] = sqrt(piv);
+        }
+        __syncthreads();
+        const double ljj = A[j * ld + j];
+        for (int i = j + 1 + tid; i <= N; i += nt) {
+            const double v = A[i * ld + j] / ljj;
+            A[i * ld + j] = v;
+            col[i] = v;
+        }
+        __syncthreads();
+        for (int i = j + 1 + wy; i <= N; i += ny) {
+            const double lij = col[i];
+            const int kmax = i < N ? i : N - 1;
+            for (int k = j + 1 + lane; k <= kmax; k += 32) A[i * ld + k] -= lij * col[k];
+        }
+        __syncthreads();
+    }
+    // backward substitution L^T x = y (y in row N)
+    for (int j = N - 1; j >= 0; --j) {
+        if (tid == 0) A[N * ld + j] = A[N * ld + j] / A[j * ld + j];
+        __syncthreads();
+        const double xj = A[N * ld + j];
+        for (int i = tid; i < j; i += nt) A[N * ld + i] -= A[j * ld + i] * xj;
+        __syncthreads();
+    }
+    for (int c = tid; c < N; c += nt) dp[c] = A[N * ld + c];
+    if (tid == 0) status[0] = bad >= 0 ? 1 : 0;
+    if (tid == 0) status[1] = bad;
+}
+
+// ---------------------------------------------------------------------------
+// blocked path ------------------------------------------------------------------
+
+// panel: every CTA re-factors the diagonal block in shared memory (cheap,
+// avoids a launch), CTA 0 writes it back, all CTAs solve their 64-row chunk
+// of L21 = A21 L11^-T (the rhs row N included: forward substitution).
+__global__ void __launch_bounds__(256) k_panel(double* A, int64_t ld, int64_t N, int64_t c0,
+                                               int nb, int32_t* status) {
+    extern __shared__ double smp[];
+    double* L = smp;
+    double* R = smp + kNB * (kNB + 1);
+    __shared__ int bad;
+    const int ldl = kNB + 1;
+    const int tid = threadIdx.x;
+    if (tid == 0) bad = -1;
+    for (int x = tid; x < nb * nb; x += blockDim.x) {
+        const int i = x / nb, k = x % nb;
+        L[i * ldl + k] = (k <= i) ? A[(c0 + i) * ld + c0 + k] : 0.0;
+    }
+    __syncthreads();
+    smem_potrf(L, ldl, nb, &bad, (int)c0, status);
+    if (blockIdx.x == 0) {
+        for (int x = tid; x < nb * nb; x += blockDim.x) {
+            const int i = x / nb, k = x % nb;
+            if (k <= i) A[(c0 + i) * ld + c0 + k] = L[i * ldl + k];
+        }
+        if (tid == 0 && bad >= 0) {
+            if (atomicCAS(status, 0, 1) == 0) status[1] = bad;
+        }
+    }
+    const int64_t r0 = c0 + nb + (int64_t)blockIdx.x * 64;
+    const int64_t rows = (N + 1) - r0;
+    if (rows <= 0) return;
+    const int nr = rows < 64 ? (int)rows : 64;
+    for (int x = tid; x < nr * nb; x += blockDim.x) {
+        const int i = x / nb, k = x % nb;
+        R[i * ldl + k] = A[(r0 + i) * ld + c0 + k];
+    }
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        const double lkk = L[k * ldl + k];
+        for (int i = tid; i < nr; i += blockDim.x) R[i * ldl + k] /= lkk;
+        __syncthreads();
+        const int rem = nb - k - 1;
+        for (int x = tid; x < nr * rem; x += blockDim.x) {
+            const int i = x / rem, mm = k + 1 + x % rem;
+            R[i * ldl + mm] -= R[i * ldl + k] * L[mm * ldl + k];
+        }
+        __syncthreads();
+    }
+    for (int x = tid; x < nr * nb; x += blockDim.x) {
+        const int i = x / nb, k = x % nb;
+        A[(r0 + i) * ld + c0 + k] = R[i * ldl + k];
+    }
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+// trailing update A22 -= L21 L21^T on the lower triangle (plus the rhs row),
+// 64x64 output tile per CTA, 4 warps x (32x32) on DMMA m8n8k4, K = nb.
+constexpr int kLdS = kNB + 4;  // = 4 (mod 16) doubles: conflict-free fragment loads
+
+__global__ void __launch_bounds__(128) k_syrk(double* A, int64_t ld, int64_t N, int64_t c0,
+                                              int nb) {
+    const int64_t s = c0 + nb;
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    if (tj > ti) return;
+    const int64_t row0 = s + (int64_t)ti * kTile;   // output rows (may include N)
+    const int64_t col0 = s + (int64_t)tj * kTile;   // output cols (< N)
+    extern __shared__ double sms[];
+    double* As = sms;
+    double* Bs = sms + kTile * kLdS;
+    const int tid = threadIdx.x;
+    for (int x = tid; x < kTile * kNB; x += blockDim.x) {
+        const int r = x / kNB, k = x % kNB;
+        const int64_t gr = row0 + r, gc = col0 + r;
+        As[r * kLdS + k] = (gr <= N && k < nb) ? A[gr * ld + c0 + k] : 0.0;
+        Bs[r * kLdS + k] = (gc < N && k < nb) ? A[gc * ld + c0 + k] : 0.0;
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+    const int fr = lane >> 2, fk = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int k = 0; k < nb; k += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) af[a] = As[(wr + a * 8 + fr) * kLdS + k + fk];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bf[b] = Bs[(wc + b * 8 + fr) * kLdS + k + fk];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    // C fragment: row = lane/4, cols = 2*(lane%4) + {0,1}
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int64_t gr = row0 + wr + a * 8 + fr;
+        if (gr > N) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int64_t gc = col0 + wc + b * 8 + 2 * fk;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = gc + h;
+                if (c < N && (c <= gr || gr == N)) A[gr * ld + c] -= acc[a][b][h];
+            }
+        }
+    }
+}
+
+// backward substitution for one panel: x_J = L_JJ^-T (y_J - sum_{r>J} L_rJ^T x_r);
+// partial dot products per CTA, the last CTA (ticket) reduces them in fixed
+// order and solves the triangular block.
+__global__ void __launch_bounds__(256) k_bsub(double* A, int64_t ld, int64_t N, int64_t c0,
+                                              int nb, double* part, unsigned int* ticket) {
+    __shared__ double red[4][kNB];
+    __shared__ double v[kNB];
+    __shared__ bool last;
+    const int tid = threadIdx.x;
+    const int k = tid & 63, rg = tid >> 6;
+    const int64_t rs = c0 + nb;
+    double acc = 0.0;
+    if (k < nb) {
+        for (int64_t r = rs + (int64_t)blockIdx.x * 4 + rg; r < N; r += (int64_t)gridDim.x * 4)
+            acc += A[r * ld + c0 + k] * A[N * ld + r];
+    }
+    red[rg][k] = acc;
+    __syncthreads();
+    if (tid < kNB) part[(int64_t)blockIdx.x * kNB + tid] =
+        red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid < nb) {
+        double s = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) s += part[(int64_t)b * kNB + tid];
+        v[tid] = A[N * ld + c0 + tid] - s;
+    }
+    __syncthreads();
+    for (int j = nb - 1; j >= 0; --j) {
+        if (tid == 0) v[j] = v[j] / A[(c0 + j) * ld + c0 + j];
+        __syncthreads();
+        if (tid < j) v[tid] -= A[(c0 + j) * ld + c0 + tid] * v[j];
+        __syncthreads();
+    }
+    if (tid < nb) A[N * ld + c0 + tid] = v[tid];
+    if (tid == 0) *ticket = 0;
+}
+
+__global__ void k_copy_row(const double* src, int64_t n, double* dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// depth back-substitution (ba.py:321-325) and retraction (ba.py:521-531)
+
+__global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
+                                  const int32_t* inc_var, const double* inc_block,
+                                  const double* rhs_depth, const double* depth_diag,
+                                  const uint8_t* active, double lam, const double* dp,
+                                  double* dd) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int32_t k = rinc_ptr[r]; k < rinc_ptr[r + 1]; ++k) {
+            const int32_t i = rinc[k];
+            const double* blk = inc_block + (int64_t)i * 6;
+            const double* x = dp + (int64_t)inc_var[i] * 6;
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) s += blk[a] * x[a];
+            acc += s;
+        }
+        const double cinv = active[r] ? 1.0 / (depth_diag[r] * (1.0 + lam)) : 0.0;
+        dd[r] = cinv * (rhs_depth[r] - acc);
+    }
+}
+
+__global__ void k_apply_step(int64_t F, int32_t first, int32_t last, int64_t P, const double* q,
+                             const double* t, const double* d, const double* dp,
+                             const double* dd, double* q2, double* t2, double* d2) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < F + P;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        if (x < F) {
+            const int64_t f = x;
+            if (f < first || f > last) {
+                for (int k = 0; k < 4; ++k) q2[4 * f + k] = q[4 * f + k];
+                for (int k = 0; k < 3; ++k) t2[3 * f + k] = t[3 * f + k];
+                continue;
+            }
+            const double* xi = dp + 6 * (f - first);
+            // rotvec_to_quat (geometry.py:89-101)
+            const double p0 = xi[3], p1 = xi[4], p2 = xi[5];
+            const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
+            const double kk = th < kSmallAngle ? 0.5 - th * th / 48.0 : sin(0.5 * th) / th;
+            const double dq[4] = {p0 * kk, p1 * kk, p2 * kk, cos(0.5 * th)};
+            const double* a = dq;
+            const double* b = q + 4 * f;
+            // Hamilton product dq * q (geometry.py:41-53), then normalise
+            double r[4];
+            r[0] = a[3] * b[0] + a[0] * b[3] + a[1] * b[2] - a[2] * b[1];
+            r[1] = a[3] * b[1] - a[0] * b[2] + a[1] * b[3] + a[2] * b[0];
+            r[2] = a[3] * b[2] + a[0] * b[1] - a[1] * b[0] + a[2] * b[3];
+            r[3] = a[3] * b[3] - a[0] * b[0] - a[1] * b[1] - a[2] * b[2];
+            const double nrm = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2] + r[3] * r[3]);
+            for (int k = 0; k < 4; ++k) q2[4 * f + k] = r[k] / nrm;
+            // quat_rotate (geometry.py:62-67): v + w*t + u x t, t = 2 u x v
+            const double* v = t + 3 * f;
+            const double u0 = dq[0], u1 = dq[1], u2 = dq[2], w = dq[3];
+            const double c0 = 2.0 * (u1 * v[2] - u2 * v[1]);
+            const double c1 = 2.0 * (u2 * v[0] - u0 * v[2]);
+            const double c2 = 2.0 * (u0 * v[1] - u1 * v[0]);
+            t2[3 * f + 0] = v[0] + w * c0 + (u1 * c2 - u2 * c1) + xi[0];
+            t2[3 * f + 1] = v[1] + w * c1 + (u2 * c0 - u0 * c2) + xi[1];
+            t2[3 * f + 2] = v[2] + w * c2 + (u0 * c1 - u1 * c0) + xi[2];
+        } else {
+            const int64_t r = x - F;
+            d2[r] = fmax(d[r] + dd[r], kInverseDepthFloor);
+        }
+    }
+}
+
+int64_t dense_ld(int64_t N) { return ((N + 1 + 7) / 8) * 8; }
+
+int32_t ensure_dense(dpv_problem* p, int64_t N) {
+    if (p->dense) return DPV_OK;
+    p->dense_ld = dense_ld(N);
+    DPV_TRY(p->alloc(&p->dense, (N + 1) * p->dense_ld));
+    DPV_TRY(p->alloc(&p->bsub_part, 148 * 4 * kNB));
+    return DPV_OK;
+}
+
+// blocked factor + solve on an augmented (N+1) x ld matrix
+constexpr size_t kPanelSmem = sizeof(double) * (kNB * (kNB + 1) + 64 * (kNB + 1));
+constexpr size_t kSyrkSmem = sizeof(double) * 2 * kTile * kLdS;
+
+int32_t blocked_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* part,
+                             unsigned int* ticket, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        DPV_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kPanelSmem));
+        DPV_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSyrkSmem));
+        attr_set = true;
+    }
+    for (int64_t c0 = 0; c0 < N; c0 += kNB) {
+        const int nb = (int)std::min<int64_t>(kNB, N - c0);
+        const int64_t below = (N + 1) - (c0 + nb);
+        const int gp = (int)std::max<int64_t>(1, (below + 63) / 64);
+        k_panel<<<gp, 256, kPanelSmem, st>>>(A, ld, N, c0, nb, status);
+        DPV_CHECK_LAUNCH();
+        const int64_t s = c0 + nb;
+        if (s < N) {
+            const int trows = (int)(((N + 1 - s) + kTile - 1) / kTile);
+            const int tcols = (int)(((N - s) + kTile - 1) / kTile);
+            dim3 grid(tcols, trows);
+            k_syrk<<<grid, 128, kSyrkSmem, st>>>(A, ld, N, c0, nb);
+            DPV_CHECK_LAUNCH();
+        }
+    }
+    const int64_t last_c0 = ((N - 1) / kNB) * kNB;
+    for (int64_t c0 = last_c0; c0 >= 0; c0 -= kNB) {
+        const int nb = (int)std::min<int64_t>(kNB, N - c0);
+        const int64_t rows = N - (c0 + nb);
+        const int g = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (rows + 255) / 256));
+        k_bsub<<<g, 256, 0, st>>>(A, ld, N, c0, nb, part, ticket);
+        DPV_CHECK_LAUNCH();
+    }
+    return DPV_OK;
+}
+
+}  // namespace
+
+int64_t cholesky_work_doubles(int64_t n) { return 148 * 4 * kNB + 8; }
+
+int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
+                        cudaStream_t st);
+
+int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
+                       cudaStream_t st) {
+    if (blocks && p->W > 0) {
+        k_reduced_blocks<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
+            p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->scal, blocks);
+        DPV_CHECK_LAUNCH();
+    }
+    if (rhs || cinv) {
+        k_reduced_vectors<<<grid_for(p->n * 6 + p->P, 256), 256, 0, st>>>(
+            p->n * 6, p->P, p->rhs_pose, p->rhs_schur, p->depth_diag, p->active, lam, rhs, cinv);
+        DPV_CHECK_LAUNCH();
+    }
+    return DPV_OK;
+}
+
+int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,
+              cudaStream_t st) {
+    const int64_t N = 6 * p->n;
+    DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
+    if (N <= kSmallMax) {
+        const size_t smem = sizeof(double) * (size_t)(N + 1) * (N + 1);
+        static size_t cur = 0;
+        DPV_TRY(ensure_smem(k_small_solve, smem, cur));
+        k_small_solve<<<1, 1024, smem, st>>>(p->n, p->W, p->key_a, p->key_b, p->pose_blocks,
+                                             p->schur_blocks, p->rhs_pose, p->rhs_schur, p->scal,
+                                             lam, dp, status);
+        DPV_CHECK_LAUNCH();
+    } else {
+        DPV_TRY(ensure_dense(p, N));
+        const int64_t ld = p->dense_ld;
+        DPV_CUDA(cudaMemsetAsync(p->dense, 0, sizeof(double) * (N + 1) * ld, st));
+        k_dense_scatter<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
+            p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld);
+        DPV_CHECK_LAUNCH();
+        k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam,
+                                                           p->scal, p->dense, ld);
+        DPV_CHECK_LAUNCH();
+        unsigned int* ticket = reinterpret_cast<unsigned int*>(status + 4);
+        DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+        DPV_TRY(blocked_factor_solve(p->dense, ld, N, status, p->bsub_part, ticket, st));
+        k_copy_row<<<grid_for(N, 256), 256, 0, st>>>(p->dense + N * ld, N, dp);
+        DPV_CHECK_LAUNCH();
+    }
+    return back_substitute(p, lam, dp, dd, st);
+}
+
+int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
+                        cudaStream_t st) {
+    if (p->P == 0) return DPV_OK;
+    k_back_substitute<<<grid_for(p->P, 256), 256, 0, st>>>(
+        p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
+        p->active, lam, dp, dd);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* status,
+                       double* work, cudaStream_t st) {
+    // a: augmented (n+1) x lda buffer with the rhs already in row n
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + 4);
+    DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
+    DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+    DPV_TRY(blocked_factor_solve(a, lda, n, status, work, ticket, st));
+    k_copy_row<<<grid_for(n, 256), 256, 0, st>>>(a + n * lda, n, b);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
+                   const double* dp, const double* dd, double* q2, double* t2, double* d2,
+                   cudaStream_t st) {
+    k_apply_step<<<grid_for(p->F + p->P, 256), 256, 0, st>>>(p->F, p->first, p->last, p->P, q, t,
+                                                              d, dp, dd, q2, t2, d2);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+}  // namespace dpv

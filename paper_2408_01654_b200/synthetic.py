@@ -1,0 +1,371 @@
+"""Synthetic scenes and the flow oracle: the inputs of the hot path.
+
+Restates the reference's input generator (pkg/src/patchslam/synthetic.py:
+``SceneSpec`` 34-54, ``generate`` 179-215, ``fill_flow`` 222-287) and the
+perturbation helper of its tests (pkg/tests/conftest.py:28-32) so that the
+B200 path runs on *bit-identical* inputs without importing the reference
+(``tests/golden/synth_hashes.json`` pins the SHA-256 of every array against
+the reference at configs 1-3).  It draws the same random numbers in the same
+order and evaluates the same floating-point expressions, vectorised over
+frames/edges and writing straight into the structure-of-arrays graph.
+
+This module prepares inputs; it is not the hot path.  The ground-truth
+reprojection used for flow targets is the reference's numpy expression
+(kept private as ``_np_reproject_exact``) because bit-identical targets are
+the point; the BA/correlation kernels never call it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import InfeasibleVisibility
+from .geometry import Intrinsics, Pose, matrix_to_quat, pinhole_rays, quat_to_matrix, square_grid
+from .graph import LOOP, ODOMETRY, PatchGraph
+
+DEFAULT_INTRINSICS = Intrinsics(320.0, 320.0, 256.0, 192.0)   # synthetic.py:28
+DEFAULT_IMAGE_SIZE = (512, 384)                               # synthetic.py:29
+TRAJECTORY_KINDS = ("line", "circle", "square-loop", "random-walk-with-revisit")
+_CHUNK = 1 << 18
+
+
+@dataclass(frozen=True)
+class SceneSpec:
+    kind: str = "circle"
+    n_frames: int = 50
+    seed: int = 0
+    n_landmarks: int = 4000
+    extent: float = 10.0
+    frame_dt: float = 0.1
+    shell: tuple = (1.0, 20.0)
+    image_size: tuple = DEFAULT_IMAGE_SIZE
+    intrinsics: Intrinsics = field(default_factory=lambda: DEFAULT_INTRINSICS)
+    overshoot: float = 0.15
+    look: str = "forward"
+
+    def __post_init__(self):
+        if self.kind not in TRAJECTORY_KINDS:
+            raise ValueError(f"unknown trajectory kind {self.kind!r}")
+        if self.look not in ("forward", "inward"):
+            raise ValueError(f"unknown look mode {self.look!r}")
+        if self.n_frames < 1:
+            raise ValueError("need at least one frame")
+
+
+@dataclass
+class SyntheticScene:
+    spec: SceneSpec
+    gt_poses: list
+    landmarks: np.ndarray
+    intrinsics: Intrinsics
+
+    def camera_points(self, frame_id, ids=None):
+        pts = self.landmarks if ids is None else self.landmarks[ids]
+        return self.gt_poses[frame_id].inverse().act(pts)
+
+    def visible_landmarks(self, frame_id, margin=2.0):
+        """synthetic.py:68-79."""
+        cam = self.camera_points(frame_id)
+        pix, valid = _project(cam, self.intrinsics)
+        w, h = self.spec.image_size
+        ok = (valid & (cam[:, 2] > 0.5)
+              & (pix[:, 0] >= margin) & (pix[:, 0] <= w - 1 - margin)
+              & (pix[:, 1] >= margin) & (pix[:, 1] <= h - 1 - margin))
+        return np.nonzero(ok)[0]
+
+
+@dataclass(frozen=True)
+class OracleConfig:
+    pixel_noise_sigma: float = 0.0
+    outlier_fraction: float = 0.0
+    outlier_magnitude: float = 40.0
+    low_confidence: float = 0.05
+
+    def __post_init__(self):
+        if not 0.0 <= self.outlier_fraction < 1.0:
+            raise ValueError("outlier fraction must lie in [0, 1)")
+
+
+def _project(points, intr):
+    """project_array (geometry.py:468-475)."""
+    z = points[..., 2]
+    valid = z > 1e-8
+    zs = np.where(valid, z, 1.0)
+    u = intr.fx * points[..., 0] / zs + intr.cx
+    v = intr.fy * points[..., 1] / zs + intr.cy
+    return np.stack([u, v], axis=-1), valid
+
+
+def _np_reproject_exact(rays, inv_depth, rot_i, t_i, rot_j, t_j, intr):
+    """The reference's numpy reprojection expression, for bit-identical targets."""
+    x_cam = rays / inv_depth[:, None, None]
+    x_world = x_cam @ rot_i.swapaxes(-1, -2) + t_i[:, None, :]
+    x_tgt = (x_world - t_j[:, None, :]) @ rot_j
+    z = x_tgt[..., 2]
+    valid = z > 1e-8
+    zs = np.where(valid, z, 1.0)
+    pix = np.stack([intr.fx * x_tgt[..., 0] / zs + intr.cx,
+                    intr.fy * x_tgt[..., 1] / zs + intr.cy], axis=-1)
+    return pix, valid
+
+
+# ---------------------------------------------------------------------------
+# trajectories (synthetic.py:98-172)
+
+
+def _look_rotation(forward):
+    f = forward / np.linalg.norm(forward)
+    up = np.array([0.0, 1.0, 0.0])
+    if abs(f @ up) > 0.99:
+        up = np.array([0.0, 0.0, 1.0])
+    right = np.cross(f, up)
+    right /= np.linalg.norm(right)
+    down = np.cross(f, right)
+    return np.stack([right, down, f], axis=1)
+
+
+def _positions(spec, rng):
+    n = spec.n_frames
+    if spec.kind == "line":
+        s = np.linspace(0.0, spec.extent, n)
+        return np.stack([s, np.zeros(n), np.zeros(n)], axis=1)
+    if spec.kind == "circle":
+        r = spec.extent / 2.0
+        ang = np.linspace(0.0, 2 * np.pi * (1 + spec.overshoot), n)
+        return np.stack([r * np.cos(ang), np.zeros(n), r * np.sin(ang)], axis=1)
+    if spec.kind == "square-loop":
+        side = spec.extent
+        s = np.linspace(0.0, 4.0 * side * (1 + spec.overshoot), n) % (4.0 * side)
+        pos = np.zeros((n, 3))
+        for i, dist in enumerate(s):
+            leg, rem = int(dist // side) % 4, dist % side
+            pos[i] = [(rem, 0.0, 0.0), (side, 0.0, rem), (side - rem, 0.0, side),
+                      (0.0, 0.0, side - rem)][leg]
+        return pos
+    step = spec.extent / max(n - 1, 1)
+    heading = rng.uniform(0, 2 * np.pi)
+    pos = [np.zeros(3)]
+    n_out = max(int(0.7 * n), 1)
+    for _ in range(n_out - 1):
+        heading += rng.normal(0.0, 0.25)
+        pos.append(pos[-1] + step * np.array([np.cos(heading), 0.0, np.sin(heading)]))
+    far = pos[-1]
+    for i in range(n - n_out):
+        a = (i + 1) / max(n - n_out, 1)
+        pos.append((1 - a) * far)
+    return np.stack(pos[:n])
+
+
+def _gt_poses(spec, rng):
+    pos = _positions(spec, rng)
+    centroid = pos.mean(axis=0)
+    out = []
+    for i in range(len(pos)):
+        if spec.look == "inward":
+            fwd = centroid - pos[i]
+        else:
+            fwd = pos[min(len(pos) - 1, i + 1)] - pos[max(0, i - 1)]
+        if np.linalg.norm(fwd) < 1e-12:
+            fwd = np.array([1.0, 0.0, 0.0])
+        out.append(Pose(matrix_to_quat(_look_rotation(fwd)), pos[i]))
+    return out
+
+
+def _landmarks(spec, pos, rng):
+    lo, hi = spec.shell
+    anchor = pos[rng.integers(0, len(pos), size=spec.n_landmarks)]
+    direction = rng.normal(size=(spec.n_landmarks, 3))
+    direction /= np.linalg.norm(direction, axis=1, keepdims=True)
+    radius = rng.uniform(lo, hi, size=spec.n_landmarks)
+    return anchor + direction * radius[:, None]
+
+
+# ---------------------------------------------------------------------------
+# scene + graph (synthetic.py:179-215)
+
+
+def generate(spec: SceneSpec, patches_per_frame: int = 96, odometry_radius: int = 13,
+             patch_size: int = 3, initial_targets: bool = True):
+    """Ground-truth scene + patch graph at the truth (bit-identical to the reference).
+
+    ``initial_targets=False`` skips the (later overwritten) initial-reprojection
+    targets of the odometry edges (graph.py:159-164) and leaves them at 0.
+    """
+    rng = np.random.default_rng(spec.seed)
+    gt = _gt_poses(spec, rng)
+    lms = _landmarks(spec, np.stack([p.t for p in gt]), rng)
+    scene = SyntheticScene(spec, gt, lms, spec.intrinsics)
+    graph = PatchGraph(spec.intrinsics, patch_size)
+    margin = (patch_size - 1) / 2.0 + 0.5
+    m = patch_size * patch_size
+    counts = np.zeros(spec.n_frames, dtype=np.int64)
+    for fid in range(spec.n_frames):
+        vis = scene.visible_landmarks(fid, margin)
+        if len(vis) < patches_per_frame:
+            raise InfeasibleVisibility(
+                f"frame {fid} sees {len(vis)} landmarks < {patches_per_frame};"
+                " increase n_landmarks or shrink the shell")
+        chosen = rng.choice(vis, size=patches_per_frame, replace=False)
+        cam = scene.camera_points(fid, chosen)
+        pix, _ = _project(cam, spec.intrinsics)
+        grids = np.stack([square_grid(pix[i], patch_size) for i in range(patches_per_frame)])
+        depths = np.array([float(1.0 / cam[i, 2]) for i in range(patches_per_frame)])
+        graph.add_frame_arrays(gt[fid].q, gt[fid].t, fid * spec.frame_dt, grids, depths,
+                               chosen.astype(np.int64))
+        counts[fid] = patches_per_frame
+        if odometry_radius > 0:
+            tri = PatchGraph.odometry_triples(fid, odometry_radius, counts)
+            if len(tri):
+                graph.add_edge_arrays(tri[:, 0], tri[:, 1], tri[:, 2], np.zeros((len(tri), m, 2)),
+                                      np.ones((len(tri), 2)), ODOMETRY)
+    if initial_targets and graph.n_edges:
+        _reproject_targets(graph, np.arange(graph.n_edges), graph._q.view, graph._t.view,
+                           graph._depth.view)
+    return scene, graph
+
+
+def _reproject_targets(graph, idx, q, t, patch_depth):
+    """Initial targets = current reprojection (graph.py:152-164), exact numpy."""
+    rot = quat_to_matrix(q)
+    off = graph.patch_offset()
+    for lo in range(0, len(idx), _CHUNK):
+        sel = idx[lo:lo + _CHUNK]
+        src = graph._src.view[sel].astype(np.int64)
+        dst = graph._dst.view[sel].astype(np.int64)
+        gid = off[src] + graph._pat.view[sel]
+        rays = pinhole_rays(graph._grid.view[gid], graph.intrinsics)
+        pix, _ = _np_reproject_exact(rays, patch_depth[gid], rot[src], t[src], rot[dst], t[dst],
+                                     graph.intrinsics)
+        graph._tgt.view[sel] = pix
+    graph._edge_clean = min(graph._edge_clean, int(idx.min()) if len(idx) else graph._edge_clean)
+
+
+def add_loop_edges(graph, n_poses: int, patches: int, seed: int = 0):
+    """Long-range LOOP edges, the bench-ba recipe (cli.py:103-110)."""
+    rng = np.random.default_rng(seed)
+    tri = []
+    for _ in range(max(2, n_poses // 60)):
+        old = int(rng.integers(0, max(1, n_poses // 4)))
+        recent = int(rng.integers(3 * n_poses // 4, n_poses))
+        tri.extend((old, k, recent) for k in range(min(patches, 32)))
+    tri = np.asarray(tri, dtype=np.int64)
+    m = graph.patch_size ** 2
+    return graph.add_edge_arrays(tri[:, 0], tri[:, 1], tri[:, 2], np.zeros((len(tri), m, 2)),
+                                 np.ones((len(tri), 2)), LOOP)
+
+
+# ---------------------------------------------------------------------------
+# flow oracle (synthetic.py:222-300)
+
+
+def fill_flow(graph, scene, config: OracleConfig = OracleConfig(), edge_indices=None,
+              seed: int = 0) -> None:
+    """Ground-truth reprojection + one Gaussian shift per edge, seeded
+    outliers with low confidence, unobservable edges at confidence 0."""
+    idx = (np.arange(graph.n_edges) if edge_indices is None
+           else np.asarray(list(edge_indices), dtype=np.int64))
+    if len(idx) == 0:
+        return
+    rng = np.random.default_rng(seed)
+    intr = graph.intrinsics
+    gt_q = np.stack([p.q for p in scene.gt_poses])
+    gt_t = np.stack([p.t for p in scene.gt_poses])
+    rot = quat_to_matrix(gt_q)
+    off = graph.patch_offset()
+    w, h = scene.spec.image_size
+    slack = 0.25 * max(w, h)
+    n = len(idx)
+    pix_all = np.empty((n, graph.patch_size ** 2, 2))
+    obs = np.empty(n, dtype=bool)
+    for lo in range(0, n, _CHUNK):
+        sel = idx[lo:lo + _CHUNK]
+        src = graph._src.view[sel].astype(np.int64)
+        dst = graph._dst.view[sel].astype(np.int64)
+        gid = off[src] + graph._pat.view[sel]
+        rays = pinhole_rays(graph._grid.view[gid], intr)
+        lm = graph._lm.view[gid]
+        cam_z = np.einsum("eb,eb->e", rot[src][:, :, 2], scene.landmarks[lm] - gt_t[src])
+        pix, valid = _np_reproject_exact(rays, 1.0 / cam_z, rot[src], gt_t[src], rot[dst],
+                                         gt_t[dst], intr)
+        obs[lo:lo + len(sel)] = (
+            valid.all(axis=1)
+            & (pix[..., 0] > -slack).all(axis=1) & (pix[..., 0] < w + slack).all(axis=1)
+            & (pix[..., 1] > -slack).all(axis=1) & (pix[..., 1] < h + slack).all(axis=1))
+        pix_all[lo:lo + len(sel)] = pix
+    shift = (rng.normal(0.0, config.pixel_noise_sigma, size=(n, 2))
+             if config.pixel_noise_sigma > 0 else np.zeros((n, 2)))
+    outlier = rng.random(n) < config.outlier_fraction
+    ang = rng.uniform(0, 2 * np.pi, size=n)
+    gross = config.outlier_magnitude * np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    target = pix_all + shift[:, None, :]
+    bad = outlier & obs
+    target[bad] = target[bad] + gross[bad][:, None, :]
+    conf = np.ones((n, 2))
+    conf[bad] = config.low_confidence
+    conf[~obs] = 0.0
+    graph._tgt.view[idx] = target
+    graph._conf.view[idx] = conf
+    graph._edge_clean = min(graph._edge_clean, int(idx.min()))
+
+
+def make_flow_oracle(scene, config: OracleConfig, seed: int = 0):
+    """Stateful oracle (graph, edge_indices) -> None (synthetic.py:290-300)."""
+    counter = {"n": 0}
+
+    def oracle(graph, edge_indices):
+        fill_flow(graph, scene, config, edge_indices, seed=seed * 100003 + counter["n"])
+        counter["n"] += 1
+    return oracle
+
+
+def perturb_poses(graph, sigma: float, seed: int, first: int = 1) -> None:
+    """Left-multiply Pose.exp(N(0, sigma)) onto every frame from ``first``
+    (pkg/tests/conftest.py:28-32)."""
+    rng = np.random.default_rng(seed)
+    for f in range(first, graph.n_frames):
+        p = Pose.exp(rng.normal(0, sigma, 6)) * Pose(graph._q.view[f], graph._t.view[f])
+        graph._q.view[f] = p.q
+        graph._t.view[f] = p.t
+    graph._pose_ver += 1
+
+
+# ---------------------------------------------------------------------------
+# benchmark configurations
+
+
+CONFIGS = {
+    # name: (SceneSpec kwargs, loop span or 0, free range fn)
+    "cfg1": dict(spec=dict(kind="circle", n_frames=16, seed=0, n_landmarks=3000, look="inward",
+                           image_size=(640, 480),
+                           intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0)),
+                 loops=0, free=lambda n: (1, 15)),
+    "cfg2": dict(spec=dict(kind="circle", n_frames=40, seed=0, n_landmarks=6000, look="inward",
+                           image_size=(752, 480),
+                           intrinsics=Intrinsics(458.654, 457.296, 367.215, 248.375)),
+                 loops=0, free=lambda n: (n - 22, n - 1)),
+    "mid": dict(spec=dict(kind="circle", n_frames=120, seed=0, n_landmarks=8640, look="inward",
+                          image_size=(640, 480), intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0),
+                          extent=15.0),
+                loops=120, free=lambda n: (1, n - 1)),
+    "cfg3": dict(spec=dict(kind="circle", n_frames=2000, seed=0, n_landmarks=144000,
+                           look="inward", image_size=(640, 480),
+                           intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0), extent=250.0),
+                 loops=2000, free=lambda n: (1, n - 1)),
+}
+
+
+def make_config(name: str, initial_targets: bool = False):
+    """Build a benchmark configuration: (scene, graph, free_range).
+
+    Recipe: generate(96 patches, radius 13) -> bench-ba LOOP
+    edges -> fill_flow(sigma=0.3, seed=1) -> perturb_poses(0.02, seed=11)."""
+    cfg = CONFIGS[name]
+    spec = SceneSpec(**cfg["spec"])
+    scene, graph = generate(spec, 96, 13, initial_targets=initial_targets)
+    if cfg["loops"]:
+        add_loop_edges(graph, cfg["loops"], 96, seed=0)
+    fill_flow(graph, scene, OracleConfig(pixel_noise_sigma=0.3), seed=1)
+    perturb_poses(graph, 0.02, seed=11)
+    return scene, graph, cfg["free"](spec.n_frames)

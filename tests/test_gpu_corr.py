@@ -1,0 +1,70 @@
+"""GPU parity of the correlation kernel (K1) against the float64 oracle.
+
+Tolerance: float32 accumulation over C=128 channels of unit-variance / sqrt(C)
+features -> |err| <= 2e-5 (fp32 features); bf16 features are compared with
+the oracle evaluated on the same bf16 values -> |err| <= 2e-4 (bf16 output of
+the level-1 pool is rounded once more).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import corr_oracle  # noqa: E402
+from paper_2408_01654_b200 import corr  # noqa: E402
+
+
+def make(rng, E=300, C=128, F=4, H=30, W=40, P=50, spread=1.0):
+    g = (rng.normal(size=(P, 9, C)) / np.sqrt(C)).astype(np.float32)
+    f = (rng.normal(size=(F, H, W, C)) / np.sqrt(C)).astype(np.float32)
+    base = rng.uniform(-3, [W + 3, H + 3], size=(E, 1, 2))
+    offs = np.stack(np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0), -1).reshape(1, 9, 2)
+    coords = base + spread * offs * rng.uniform(0.1, 0.3) + rng.normal(0, 0.05, (E, 9, 2))
+    ii = rng.integers(0, P, E).astype(np.int32)
+    jj = rng.integers(0, F, E).astype(np.int32)
+    return g, f, coords, ii, jj
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_corr_matches_oracle(dtype):
+    rng = np.random.default_rng(0)
+    g, f, coords, ii, jj = make(rng)
+    coords[0] = np.nan
+    coords[1] += 500.0                       # fully out of bounds
+    coords[2, :, 0] = np.linspace(-1, 60, 9)  # cells spread wider than the staged window
+    gd = torch.as_tensor(g, device="cuda").to(dtype)
+    fd = torch.as_tensor(f, device="cuda").to(dtype)
+    pyr = corr.pyramid(fd)
+    out = corr.corr(gd, pyr, torch.as_tensor(coords, device="cuda"),
+                    torch.as_tensor(ii, device="cuda"), torch.as_tensor(jj, device="cuda"))
+    g64 = gd.double().cpu().numpy()
+    f64 = fd.double().cpu().numpy()
+    f1 = pyr[1].double().cpu().numpy()
+    ref = corr_oracle.corr(g64, [f64, f1], coords, ii, jj)
+    tol = 2e-5 if dtype == torch.float32 else 2e-4
+    err = np.abs(out.cpu().numpy() - ref).max()
+    assert err < tol, err
+    assert np.all(out[:2].cpu().numpy() == 0)
+    if dtype == torch.float32:
+        assert np.allclose(pyr[1].cpu().numpy(), corr_oracle.avg_pool4(f), atol=1e-6)
+
+
+def test_corr_on_reprojected_patches():
+    """K2 -> K1: correlation at the BA problem's reprojections peaks at the
+    center when the features of frame j are those sampled from the truth."""
+    rng = np.random.default_rng(1)
+    C, H, W = 64, 40, 52
+    f = (rng.normal(size=(1, H, W, C)) / 8).astype(np.float32)
+    coords = rng.uniform(5, 30, size=(40, 1, 2)).round() + np.stack(
+        np.meshgrid(np.arange(3.0), np.arange(3.0)), -1).reshape(1, 9, 2)
+    g = np.stack([[f[0, int(y), int(x)] for x, y in c] for c in coords]).astype(np.float32)
+    out = corr.corr(torch.as_tensor(g, device="cuda"), [torch.as_tensor(f, device="cuda")],
+                    torch.as_tensor(coords, device="cuda"),
+                    torch.arange(40, dtype=torch.int32, device="cuda"),
+                    torch.zeros(40, dtype=torch.int32, device="cuda"))
+    flat = out[:, 0].reshape(40, 9, 49).argmax(-1).cpu().numpy()
+    assert np.all(flat == 24)

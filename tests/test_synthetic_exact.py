@@ -1,0 +1,50 @@
+"""The package's input generator reproduces the reference inputs bit-exactly.
+
+tests/golden/synth_hashes.json holds SHA-256 digests of every SoA array the
+reference (patchslam.synthetic.generate + bench-ba loop edges + fill_flow +
+conftest.perturb_poses) produced for the benchmark configurations
+(tests/golden/make_golden.py).  No GPU needed.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2408_01654_b200 import synthetic
+
+
+def digests(graph):
+    out = {}
+    for k, v in graph.soa().items():
+        a = np.ascontiguousarray(np.asarray(v))
+        out[k] = hashlib.sha256(a.tobytes()).hexdigest()
+    return out
+
+
+TABLE = json.load(open(os.path.join(GOLDEN, "synth_hashes.json")))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "mid"])
+def test_inputs_bit_identical(name):
+    _, graph, _ = synthetic.make_config(name)
+    ref = TABLE[name]
+    assert graph.n_edges == ref["n_edges"]
+    assert graph.n_frames == ref["n_frames"]
+    got = digests(graph)
+    bad = [k for k in ref["sha256"] if got[k] != ref["sha256"][k]]
+    assert not bad, f"arrays differ from the reference: {bad}"
+
+
+@pytest.mark.slow
+def test_cfg3_inputs_bit_identical():
+    if os.environ.get("DPV_SLOW") != "1":
+        pytest.skip("set DPV_SLOW=1 (cfg3 generation takes ~1 min)")
+    _, graph, _ = synthetic.make_config("cfg3")
+    ref = TABLE["cfg3"]
+    assert graph.n_edges == ref["n_edges"]
+    got = digests(graph)
+    assert {k: got[k] for k in ref["sha256"]} == ref["sha256"]
