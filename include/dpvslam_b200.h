@@ -43,6 +43,13 @@ int32_t dpv_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor)
 /* Number of kernels this library has launched in the process (monotone counter). */
 int64_t dpv_launch_count(void);
 
+/* Per-kernel CUDA-event timing (used by bench.py for the roofline numbers):
+ * enable, run, then collect = synchronise + aggregate per kernel name
+ * ('\n'-separated names, summed ms, launch counts) and reset. */
+int32_t dpv_timing_enable(int32_t on);
+int32_t dpv_timing_collect(char* names, int64_t names_cap, double* total_ms, int64_t* counts,
+                           int32_t cap, int32_t* n_out);
+
 /* ------------------------------------------------------------------------
  * Geometry (K2 standalone).
  * ---------------------------------------------------------------------- */
@@ -144,6 +151,16 @@ int32_t dpv_reduced_system(dpv_problem* prob, double lam, double* blocks, double
  * dp (n,6), dd (P).  *status_dev (device int32) = 0 ok / 1 not positive definite. */
 int32_t dpv_solve(dpv_problem* prob, double lam, double* dp, double* dd, int32_t* status_dev,
                   void* stream);
+/* K2 pixels of every problem edge times `scale` (problem order, (E,m,2)):
+ * the reprojected coordinates P' that feed the correlation lookup (pass 0.25
+ * for 1/4-resolution feature maps).  Same arithmetic as reproject_grid. */
+int32_t dpv_reproject_coords(dpv_problem* prob, const double* q, const double* t,
+                             const double* d, double scale, double* coords, void* stream);
+/* Replace the flow targets (E,m,2) and confidences (E,2) (problem order, conf
+ * may be NULL) without rebuilding the index: the per-iteration update-operator
+ * output of DPVO or a re-run flow oracle. */
+int32_t dpv_update_targets(dpv_problem* prob, const double* target, const double* conf,
+                           void* stream);
 /* BlockSparseSystem.back_substitute(dp, lam) (ba.py:321-325): dd (P). */
 int32_t dpv_back_substitute(dpv_problem* prob, double lam, const double* dp, double* dd,
                             void* stream);

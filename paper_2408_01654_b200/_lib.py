@@ -177,3 +177,25 @@ def _torch_dtype(code):
 
 SIGNATURES["dpv_avg_pool4"] = (C.c_int32, [vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                            C.c_int32, vp, vp])
+SIGNATURES["dpv_reproject_coords"] = (C.c_int32, [vp, vp, vp, vp, C.c_double, vp, vp])
+SIGNATURES["dpv_update_targets"] = (C.c_int32, [vp, vp, vp, vp])
+SIGNATURES["dpv_timing_enable"] = (C.c_int32, [C.c_int32])
+SIGNATURES["dpv_timing_collect"] = (C.c_int32, [C.c_char_p, C.c_int64, vp, vp, C.c_int32,
+                                                c_int32_p])
+
+
+def timing_enable(on: bool) -> None:
+    check(lib().dpv_timing_enable(1 if on else 0), "timing_enable")
+
+
+def timing_collect() -> dict:
+    """{kernel name: (total ms, launches)} since the last collect (synchronises)."""
+    cap = 128
+    names = C.create_string_buffer(8192)
+    ms = (C.c_double * cap)()
+    cnt = (C.c_int64 * cap)()
+    n = C.c_int32()
+    check(lib().dpv_timing_collect(names, 8192, C.cast(ms, vp), C.cast(cnt, vp), cap, C.byref(n)),
+          "timing_collect")
+    keys = names.value.decode().split("\n")[:n.value]
+    return {k: (ms[i], int(cnt[i])) for i, k in enumerate(keys)}

@@ -137,6 +137,45 @@ __global__ void k_residuals(int64_t E, int m, int64_t P, const int32_t* a_src,
     }
 }
 
+// reprojected pixels * scale in problem-edge order (coordinates for K1)
+__global__ void k_coords(int64_t E, int m, int64_t P, const int32_t* a_src,
+                         const int32_t* a_dst, const int32_t* a_row, const int32_t* a_pidx,
+                         const double* r_ray, const double* Rall, const double* tall,
+                         const double* d, double fx, double fy, double cx, double cy,
+                         double scale, double* coords) {
+    const double intr[4] = {fx, fy, cx, cy};
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        Frame fi, fj;
+        load_frame(Rall, tall, a_src[e], fi);
+        load_frame(Rall, tall, a_dst[e], fj);
+        const int32_t row = a_row[e];
+        const double id = 1.0 / __ldg(d + row);
+        const int64_t p = a_pidx[e];
+        for (int c = 0; c < m; ++c) {
+            Cell cl;
+            reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
+                           __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr, cl);
+            coords[(p * m + c) * 2] = cl.u * scale;
+            coords[(p * m + c) * 2 + 1] = cl.v * scale;
+        }
+    }
+}
+
+// new flow targets / confidences (problem order) -> assembly-order SoA
+__global__ void k_update_targets(int64_t E, int m, const int32_t* p_pos, const double* tgt,
+                                 const double* conf, double* a_tgt, double* a_w) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = p_pos[p];
+        for (int c = 0; c < 2 * m; ++c) a_tgt[(int64_t)c * E + e] = tgt[p * 2 * m + c];
+        if (conf) {
+            a_w[e] = conf[2 * p];
+            a_w[E + e] = conf[2 * p + 1];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K2+K3 fused: one warp per segment (same source/target frame, <= kSegMax
 // edges), one lane per edge.  Per edge it writes e_pd (6), c_dd, g_d; per
@@ -409,11 +448,13 @@ __global__ void k_pin(const double* t, int32_t first_free, int32_t anchor, doubl
 int32_t objective(dpv_problem* p, const double* q, const double* t, const double* d, double* out,
                   cudaStream_t st) {
     DPV_TRY(frame_rotations(p, q, st));
+    DPV_TSTART("objective", st);
     k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
                                             p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d,
                                             p->intr[0], p->intr[1], p->intr[2], p->intr[3],
                                             p->obj_part);
     DPV_CHECK_LAUNCH();
+    DPV_TSTART("sum_parts", st);
     k_sum_parts<<<1, 1024, 0, st>>>(kObjBlocks, p->obj_part, out);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
@@ -423,10 +464,33 @@ int32_t residuals(dpv_problem* p, const double* q, const double* t, const double
                   uint8_t* valid, cudaStream_t st) {
     DPV_TRY(frame_rotations(p, q, st));
     if (p->E == 0) return DPV_OK;
+    DPV_TSTART("residuals", st);
     k_residuals<<<grid_for(p->E, 256), 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst,
                                                       p->a_row, p->a_pidx, p->a_tgt, p->r_ray,
                                                       p->frame_R, t, d, p->intr[0], p->intr[1],
                                                       p->intr[2], p->intr[3], res, valid);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t coords(dpv_problem* p, const double* q, const double* t, const double* d, double scale,
+               double* out, cudaStream_t st) {
+    DPV_TRY(frame_rotations(p, q, st));
+    if (p->E == 0) return DPV_OK;
+    DPV_TSTART("coords", st);
+    k_coords<<<grid_for(p->E, 256), 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
+                                                   p->a_pidx, p->r_ray, p->frame_R, t, d,
+                                                   p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+                                                   scale, out);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cudaStream_t st) {
+    if (p->E == 0) return DPV_OK;
+    DPV_TSTART("update_targets", st);
+    k_update_targets<<<grid_for(p->E, 256), 256, 0, st>>>(p->E, p->m, p->p_pos, tgt, conf,
+                                                           p->a_tgt, p->a_w);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
 }
@@ -441,6 +505,7 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         const int warps_per_block = 4;
         int blocks = (int)std::min<int64_t>((p->S + warps_per_block - 1) / warps_per_block,
                                             (int64_t)sm_count() * 64);
+        DPV_TSTART("assemble_edges", st);
         k_assemble_edges<<<blocks, 32 * warps_per_block, 0, st>>>(
             p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,
             p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
@@ -448,12 +513,14 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         DPV_CHECK_LAUNCH();
     }
     if (p->P > 0) {
+        DPV_TSTART("rows", st);
         k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,
                                                      p->e_terms, p->depth_diag, p->rhs_depth,
                                                      p->active, p->cinv0, grad_bits, n_inactive);
         DPV_CHECK_LAUNCH();
     }
     if (p->I > 0) {
+        DPV_TSTART("incidences", st);
         k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
                                                            p->inc_row, p->e_terms, p->cinv0,
                                                            p->inc_block, p->uinc);
@@ -461,6 +528,7 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     }
     if (p->W > 0) {
         int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
+        DPV_TSTART("key_blocks", st);
         k_key_blocks<<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
                                              p->key_pair_ptr, p->pair_l, p->pair_r, p->uinc,
                                              p->inc_block, p->pose_blocks, p->schur_blocks);
@@ -468,11 +536,13 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     }
     if (p->n > 0) {
         int blocks = (int)std::min<int64_t>((p->n + 3) / 4, (int64_t)sm_count() * 64);
+        DPV_TSTART("var_rhs", st);
         k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
                                           p->var_inc_ptr, p->inc_row, p->uinc, p->rhs_depth,
                                           p->rhs_pose, p->rhs_schur, grad_bits);
         DPV_CHECK_LAUNCH();
         if (p->scale_degenerate) {
+            DPV_TSTART("pin", st);
             k_pin<<<1, 1, 0, st>>>(t, p->first, p->touched0, p->scal);
             DPV_CHECK_LAUNCH();
         }

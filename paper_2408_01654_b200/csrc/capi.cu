@@ -17,6 +17,45 @@ std::atomic<int64_t> g_launches{0};
 void set_error(const std::string& msg) { t_error = msg; }
 void clear_error() { t_error.clear(); }
 
+// ---- per-kernel event timing ------------------------------------------------
+bool g_timing = false;
+namespace {
+struct TimerRec {
+    std::string name;
+    cudaEvent_t a, b;
+    cudaStream_t st;
+};
+std::mutex g_tmu;
+std::vector<TimerRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+std::vector<size_t> g_open;  // indices of records awaiting their stop event
+
+cudaEvent_t pool_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+void timer_push(const char* name, cudaStream_t st, bool start) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (start) {
+        TimerRec r{name, pool_event(), pool_event(), st};
+        cudaEventRecord(r.a, st);
+        g_recs.push_back(r);
+        g_open.push_back(g_recs.size() - 1);
+    } else if (!g_open.empty()) {
+        TimerRec& r = g_recs[g_open.back()];
+        g_open.pop_back();
+        cudaEventRecord(r.b, r.st);
+    }
+}
+
 int sm_count() {
     static int cached = 0;
     if (cached == 0) {
@@ -212,6 +251,53 @@ int32_t dpv_device_info(int32_t* sms, int32_t* major, int32_t* minor) {
     return DPV_OK;
 }
 
+int32_t dpv_timing_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_timing = on != 0;
+    return DPV_OK;
+}
+
+int32_t dpv_timing_collect(char* names, int64_t names_cap, double* total_ms, int64_t* counts,
+                           int32_t cap, int32_t* n_out) {
+    // synchronises the device, aggregates event pairs per kernel name, resets
+    DPV_CUDA(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_tmu);
+    std::vector<std::string> keys;
+    std::vector<double> ms;
+    std::vector<int64_t> cnt;
+    for (TimerRec& r : g_recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        while (k < keys.size() && keys[k] != r.name) ++k;
+        if (k == keys.size()) {
+            keys.push_back(r.name);
+            ms.push_back(0.0);
+            cnt.push_back(0);
+        }
+        ms[k] += t;
+        cnt[k] += 1;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    g_open.clear();
+    std::string joined;
+    const int n = (int)std::min<size_t>(keys.size(), (size_t)cap);
+    for (int k = 0; k < n; ++k) {
+        joined += keys[k];
+        joined += '\n';
+        if (total_ms) total_ms[k] = ms[k];
+        if (counts) counts[k] = cnt[k];
+    }
+    if (names && names_cap > 0) {
+        std::strncpy(names, joined.c_str(), (size_t)names_cap - 1);
+        names[names_cap - 1] = '\0';
+    }
+    if (n_out) *n_out = n;
+    return DPV_OK;
+}
+
 int32_t dpv_quat_to_matrix(const double* q, int64_t n, double* rot, void* stream) {
     clear_error();
     DPV_ARG(n >= 0 && (n == 0 || (q && rot)), "bad quat_to_matrix args");
@@ -359,6 +445,20 @@ int32_t dpv_solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* s
     clear_error();
     DPV_ARG(p && dp && (dd || p->P == 0) && status_dev, "NULL argument");
     return solve(p, lam, dp, dd, status_dev, as_stream(stream));
+}
+
+int32_t dpv_reproject_coords(dpv_problem* p, const double* q, const double* t, const double* d,
+                             double scale, double* coords_out, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && (coords_out || p->E == 0), "NULL argument");
+    return coords(p, q, t, d, scale, coords_out, as_stream(stream));
+}
+
+int32_t dpv_update_targets(dpv_problem* p, const double* target, const double* conf,
+                           void* stream) {
+    clear_error();
+    DPV_ARG(p && (target || p->E == 0), "NULL argument");
+    return update_targets(p, target, conf, as_stream(stream));
 }
 
 int32_t dpv_back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,

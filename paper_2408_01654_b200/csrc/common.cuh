@@ -34,8 +34,14 @@ struct Status {
         }                                                                           \
     } while (0)
 
+#define DPV_TSTART(name, stream)                                                    \
+    do {                                                                            \
+        if (::dpv::g_timing) ::dpv::timer_push(name, stream, true);                \
+    } while (0)
+
 #define DPV_CHECK_LAUNCH()                                                          \
     do {                                                                            \
+        if (::dpv::g_timing) ::dpv::timer_push(nullptr, nullptr, false);           \
         ::dpv::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
         cudaError_t _e = cudaGetLastError();                                        \
         if (_e != cudaSuccess) {                                                    \
@@ -60,6 +66,12 @@ struct Status {
     } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Optional per-kernel CUDA-event timing (dpv_timing_*): DPV_TSTART before a
+// launch records a start event on the launch stream, the DPV_CHECK_LAUNCH
+// that follows records the matching stop event.
+extern bool g_timing;
+void timer_push(const char* name, cudaStream_t st, bool start);
 
 inline int grid_for(int64_t n, int block, int cap = 148 * 32) {
     int64_t g = (n + block - 1) / block;

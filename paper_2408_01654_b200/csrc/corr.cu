@@ -174,6 +174,7 @@ int32_t launch_corr(const void* gmap, const void* fmap, const double* coords, co
     static size_t cur = 0;
     DPV_TRY(ensure_smem(k_corr<T>, smem, cur));
     const int grid = (int)std::min<int64_t>(E, (int64_t)sm_count() * 16);
+    DPV_TSTART("corr", st);
     k_corr<T><<<grid, 192, smem, st>>>(reinterpret_cast<const T*>(gmap),
                                         reinterpret_cast<const T*>(fmap), coords, ii, jj, E, C,
                                         H, Wd, level, levels, radius, out);
@@ -209,6 +210,7 @@ int32_t avg_pool4(const void* in, int64_t F, int H, int W, int C, int dtype, voi
                   cudaStream_t st) {
     const int64_t total = F * (H / 4) * (W / 4) * C;
     if (total == 0) return DPV_OK;
+    DPV_TSTART("avg_pool4", st);
     if (dtype == 0)
         k_avg_pool4<float><<<grid_for(total, 256), 256, 0, st>>>(
             reinterpret_cast<const float*>(in), F, H, W, C, reinterpret_cast<float*>(out));

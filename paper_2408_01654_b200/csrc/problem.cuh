@@ -147,6 +147,9 @@ int32_t residuals(dpv_problem* p, const double* q, const double* t, const double
                   double* res, uint8_t* valid, cudaStream_t st);
 int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
                  cudaStream_t st);
+int32_t coords(dpv_problem* p, const double* q, const double* t, const double* d, double scale,
+               double* out, cudaStream_t st);
+int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cudaStream_t st);
 int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
                        cudaStream_t st);
 int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,

@@ -476,6 +476,7 @@ int32_t blocked_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, 
         const int nb = (int)std::min<int64_t>(kNB, N - c0);
         const int64_t below = (N + 1) - (c0 + nb);
         const int gp = (int)std::max<int64_t>(1, (below + 63) / 64);
+        DPV_TSTART("panel", st);
         k_panel<<<gp, 256, kPanelSmem, st>>>(A, ld, N, c0, nb, status);
         DPV_CHECK_LAUNCH();
         const int64_t s = c0 + nb;
@@ -483,6 +484,7 @@ int32_t blocked_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, 
             const int trows = (int)(((N + 1 - s) + kTile - 1) / kTile);
             const int tcols = (int)(((N - s) + kTile - 1) / kTile);
             dim3 grid(tcols, trows);
+            DPV_TSTART("syrk", st);
             k_syrk<<<grid, 128, kSyrkSmem, st>>>(A, ld, N, c0, nb);
             DPV_CHECK_LAUNCH();
         }
@@ -492,6 +494,7 @@ int32_t blocked_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, 
         const int nb = (int)std::min<int64_t>(kNB, N - c0);
         const int64_t rows = N - (c0 + nb);
         const int g = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (rows + 255) / 256));
+        DPV_TSTART("bsub", st);
         k_bsub<<<g, 256, 0, st>>>(A, ld, N, c0, nb, part, ticket);
         DPV_CHECK_LAUNCH();
     }
@@ -508,11 +511,13 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
 int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
                        cudaStream_t st) {
     if (blocks && p->W > 0) {
+        DPV_TSTART("reduced_blocks", st);
         k_reduced_blocks<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
             p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->scal, blocks);
         DPV_CHECK_LAUNCH();
     }
     if (rhs || cinv) {
+        DPV_TSTART("reduced_vectors", st);
         k_reduced_vectors<<<grid_for(p->n * 6 + p->P, 256), 256, 0, st>>>(
             p->n * 6, p->P, p->rhs_pose, p->rhs_schur, p->depth_diag, p->active, lam, rhs, cinv);
         DPV_CHECK_LAUNCH();
@@ -528,6 +533,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
         const size_t smem = sizeof(double) * (size_t)(N + 1) * (N + 1);
         static size_t cur = 0;
         DPV_TRY(ensure_smem(k_small_solve, smem, cur));
+        DPV_TSTART("small_solve", st);
         k_small_solve<<<1, 1024, smem, st>>>(p->n, p->W, p->key_a, p->key_b, p->pose_blocks,
                                              p->schur_blocks, p->rhs_pose, p->rhs_schur, p->scal,
                                              lam, dp, status);
@@ -536,15 +542,18 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
         DPV_TRY(ensure_dense(p, N));
         const int64_t ld = p->dense_ld;
         DPV_CUDA(cudaMemsetAsync(p->dense, 0, sizeof(double) * (N + 1) * ld, st));
+        DPV_TSTART("dense_scatter", st);
         k_dense_scatter<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
             p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld);
         DPV_CHECK_LAUNCH();
+        DPV_TSTART("dense_pin_rhs", st);
         k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam,
                                                            p->scal, p->dense, ld);
         DPV_CHECK_LAUNCH();
         unsigned int* ticket = reinterpret_cast<unsigned int*>(status + 4);
         DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
         DPV_TRY(blocked_factor_solve(p->dense, ld, N, status, p->bsub_part, ticket, st));
+        DPV_TSTART("copy_row", st);
         k_copy_row<<<grid_for(N, 256), 256, 0, st>>>(p->dense + N * ld, N, dp);
         DPV_CHECK_LAUNCH();
     }
@@ -554,6 +563,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
 int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
                         cudaStream_t st) {
     if (p->P == 0) return DPV_OK;
+    DPV_TSTART("back_substitute", st);
     k_back_substitute<<<grid_for(p->P, 256), 256, 0, st>>>(
         p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
         p->active, lam, dp, dd);
@@ -568,6 +578,7 @@ int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* st
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
     DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
     DPV_TRY(blocked_factor_solve(a, lda, n, status, work, ticket, st));
+    DPV_TSTART("copy_row", st);
     k_copy_row<<<grid_for(n, 256), 256, 0, st>>>(a + n * lda, n, b);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
@@ -576,6 +587,7 @@ int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* st
 int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
                    const double* dp, const double* dd, double* q2, double* t2, double* d2,
                    cudaStream_t st) {
+    DPV_TSTART("apply_step", st);
     k_apply_step<<<grid_for(p->F + p->P, 256), 256, 0, st>>>(p->F, p->first, p->last, p->P, q, t,
                                                               d, dp, dd, q2, t2, d2);
     DPV_CHECK_LAUNCH();
