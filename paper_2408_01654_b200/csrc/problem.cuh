@@ -162,4 +162,7 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
 int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* status,
                        double* work, cudaStream_t st);
 int64_t cholesky_work_doubles(int64_t n);
+int64_t dense_workspace_doubles(int64_t N);
+int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* x,
+                           double* ws, cudaStream_t st);
 }  // namespace dpv

@@ -14,7 +14,6 @@
 namespace dpv {
 namespace {
 
-constexpr int kNB = 64;           // panel width (K of the DMMA contraction)
 constexpr int kSmallMax = 162;    // n <= 27 poses: single-CTA shared-memory solve
 constexpr int kTile = 64;         // SYRK output tile
 
@@ -210,169 +209,6 @@ __global__ void __launch_bounds__(1024) k_small_solve(
     if (tid == 0) status[1] = bad;
 }
 
-// ---------------------------------------------------------------------------
-// blocked path ------------------------------------------------------------------
-
-// panel: every CTA re-factors the diagonal block in shared memory (cheap,
-// avoids a launch), CTA 0 writes it back, all CTAs solve their 64-row chunk
-// of L21 = A21 L11^-T (the rhs row N included: forward substitution).
-__global__ void __launch_bounds__(256) k_panel(double* A, int64_t ld, int64_t N, int64_t c0,
-                                               int nb, int32_t* status) {
-    extern __shared__ double smp[];
-    double* L = smp;
-    double* R = smp + kNB * (kNB + 1);
-    __shared__ int bad;
-    const int ldl = kNB + 1;
-    const int tid = threadIdx.x;
-    if (tid == 0) bad = -1;
-    for (int x = tid; x < nb * nb; x += blockDim.x) {
-        const int i = x / nb, k = x % nb;
-        L[i * ldl + k] = (k <= i) ? A[(c0 + i) * ld + c0 + k] : 0.0;
-    }
-    __syncthreads();
-    smem_potrf(L, ldl, nb, &bad, (int)c0, status);
-    if (blockIdx.x == 0) {
-        for (int x = tid; x < nb * nb; x += blockDim.x) {
-            const int i = x / nb, k = x % nb;
-            if (k <= i) A[(c0 + i) * ld + c0 + k] = L[i * ldl + k];
-        }
-        if (tid == 0 && bad >= 0) {
-            if (atomicCAS(status, 0, 1) == 0) status[1] = bad;
-        }
-    }
-    const int64_t r0 = c0 + nb + (int64_t)blockIdx.x * 64;
-    const int64_t rows = (N + 1) - r0;
-    if (rows <= 0) return;
-    const int nr = rows < 64 ? (int)rows : 64;
-    for (int x = tid; x < nr * nb; x += blockDim.x) {
-        const int i = x / nb, k = x % nb;
-        R[i * ldl + k] = A[(r0 + i) * ld + c0 + k];
-    }
-    __syncthreads();
-    for (int k = 0; k < nb; ++k) {
-        const double lkk = L[k * ldl + k];
-        for (int i = tid; i < nr; i += blockDim.x) R[i * ldl + k] /= lkk;
-        __syncthreads();
-        const int rem = nb - k - 1;
-        for (int x = tid; x < nr * rem; x += blockDim.x) {
-            const int i = x / rem, mm = k + 1 + x % rem;
-            R[i * ldl + mm] -= R[i * ldl + k] * L[mm * ldl + k];
-        }
-        __syncthreads();
-    }
-    for (int x = tid; x < nr * nb; x += blockDim.x) {
-        const int i = x / nb, k = x % nb;
-        A[(r0 + i) * ld + c0 + k] = R[i * ldl + k];
-    }
-}
-
-__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-    asm volatile(
-        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(c0), "+d"(c1)
-        : "d"(a), "d"(b));
-}
-
-// trailing update A22 -= L21 L21^T on the lower triangle (plus the rhs row),
-// 64x64 output tile per CTA, 4 warps x (32x32) on DMMA m8n8k4, K = nb.
-constexpr int kLdS = kNB + 4;  // = 4 (mod 16) doubles: conflict-free fragment loads
-
-__global__ void __launch_bounds__(128) k_syrk(double* A, int64_t ld, int64_t N, int64_t c0,
-                                              int nb) {
-    const int64_t s = c0 + nb;
-    const int ti = blockIdx.y, tj = blockIdx.x;
-    if (tj > ti) return;
-    const int64_t row0 = s + (int64_t)ti * kTile;   // output rows (may include N)
-    const int64_t col0 = s + (int64_t)tj * kTile;   // output cols (< N)
-    extern __shared__ double sms[];
-    double* As = sms;
-    double* Bs = sms + kTile * kLdS;
-    const int tid = threadIdx.x;
-    for (int x = tid; x < kTile * kNB; x += blockDim.x) {
-        const int r = x / kNB, k = x % kNB;
-        const int64_t gr = row0 + r, gc = col0 + r;
-        As[r * kLdS + k] = (gr <= N && k < nb) ? A[gr * ld + c0 + k] : 0.0;
-        Bs[r * kLdS + k] = (gc < N && k < nb) ? A[gc * ld + c0 + k] : 0.0;
-    }
-    __syncthreads();
-    const int warp = tid >> 5, lane = tid & 31;
-    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
-    const int fr = lane >> 2, fk = lane & 3;
-    double acc[4][4][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int k = 0; k < nb; k += 4) {
-        double af[4], bf[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) af[a] = As[(wr + a * 8 + fr) * kLdS + k + fk];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) bf[b] = Bs[(wc + b * 8 + fr) * kLdS + k + fk];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-    }
-    // C fragment: row = lane/4, cols = 2*(lane%4) + {0,1}
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int64_t gr = row0 + wr + a * 8 + fr;
-        if (gr > N) continue;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int64_t gc = col0 + wc + b * 8 + 2 * fk;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t c = gc + h;
-                if (c < N && (c <= gr || gr == N)) A[gr * ld + c] -= acc[a][b][h];
-            }
-        }
-    }
-}
-
-// backward substitution for one panel: x_J = L_JJ^-T (y_J - sum_{r>J} L_rJ^T x_r);
-// partial dot products per CTA, the last CTA (ticket) reduces them in fixed
-// order and solves the triangular block.
-__global__ void __launch_bounds__(256) k_bsub(double* A, int64_t ld, int64_t N, int64_t c0,
-                                              int nb, double* part, unsigned int* ticket) {
-    __shared__ double red[4][kNB];
-    __shared__ double v[kNB];
-    __shared__ bool last;
-    const int tid = threadIdx.x;
-    const int k = tid & 63, rg = tid >> 6;
-    const int64_t rs = c0 + nb;
-    double acc = 0.0;
-    if (k < nb) {
-        for (int64_t r = rs + (int64_t)blockIdx.x * 4 + rg; r < N; r += (int64_t)gridDim.x * 4)
-            acc += A[r * ld + c0 + k] * A[N * ld + r];
-    }
-    red[rg][k] = acc;
-    __syncthreads();
-    if (tid < kNB) part[(int64_t)blockIdx.x * kNB + tid] =
-        red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (tid < nb) {
-        double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += part[(int64_t)b * kNB + tid];
-        v[tid] = A[N * ld + c0 + tid] - s;
-    }
-    __syncthreads();
-    for (int j = nb - 1; j >= 0; --j) {
-        if (tid == 0) v[j] = v[j] / A[(c0 + j) * ld + c0 + j];
-        __syncthreads();
-        if (tid < j) v[tid] -= A[(c0 + j) * ld + c0 + tid] * v[j];
-        __syncthreads();
-    }
-    if (tid < nb) A[N * ld + c0 + tid] = v[tid];
-    if (tid == 0) *ticket = 0;
-}
-
 __global__ void k_copy_row(const double* src, int64_t n, double* dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -454,56 +290,13 @@ int32_t ensure_dense(dpv_problem* p, int64_t N) {
     if (p->dense) return DPV_OK;
     p->dense_ld = dense_ld(N);
     DPV_TRY(p->alloc(&p->dense, (N + 1) * p->dense_ld));
-    DPV_TRY(p->alloc(&p->bsub_part, 148 * 4 * kNB));
-    return DPV_OK;
-}
-
-// blocked factor + solve on an augmented (N+1) x ld matrix
-constexpr size_t kPanelSmem = sizeof(double) * (kNB * (kNB + 1) + 64 * (kNB + 1));
-constexpr size_t kSyrkSmem = sizeof(double) * 2 * kTile * kLdS;
-
-int32_t blocked_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* part,
-                             unsigned int* ticket, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        DPV_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kPanelSmem));
-        DPV_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kSyrkSmem));
-        attr_set = true;
-    }
-    for (int64_t c0 = 0; c0 < N; c0 += kNB) {
-        const int nb = (int)std::min<int64_t>(kNB, N - c0);
-        const int64_t below = (N + 1) - (c0 + nb);
-        const int gp = (int)std::max<int64_t>(1, (below + 63) / 64);
-        DPV_TSTART("panel", st);
-        k_panel<<<gp, 256, kPanelSmem, st>>>(A, ld, N, c0, nb, status);
-        DPV_CHECK_LAUNCH();
-        const int64_t s = c0 + nb;
-        if (s < N) {
-            const int trows = (int)(((N + 1 - s) + kTile - 1) / kTile);
-            const int tcols = (int)(((N - s) + kTile - 1) / kTile);
-            dim3 grid(tcols, trows);
-            DPV_TSTART("syrk", st);
-            k_syrk<<<grid, 128, kSyrkSmem, st>>>(A, ld, N, c0, nb);
-            DPV_CHECK_LAUNCH();
-        }
-    }
-    const int64_t last_c0 = ((N - 1) / kNB) * kNB;
-    for (int64_t c0 = last_c0; c0 >= 0; c0 -= kNB) {
-        const int nb = (int)std::min<int64_t>(kNB, N - c0);
-        const int64_t rows = N - (c0 + nb);
-        const int g = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (rows + 255) / 256));
-        DPV_TSTART("bsub", st);
-        k_bsub<<<g, 256, 0, st>>>(A, ld, N, c0, nb, part, ticket);
-        DPV_CHECK_LAUNCH();
-    }
+    DPV_TRY(p->alloc(&p->bsub_part, dense_workspace_doubles(N)));
     return DPV_OK;
 }
 
 }  // namespace
 
-int64_t cholesky_work_doubles(int64_t n) { return 148 * 4 * kNB + 8; }
+int64_t cholesky_work_doubles(int64_t n) { return dense_workspace_doubles(n); }
 
 int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
                         cudaStream_t st);
@@ -550,12 +343,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
         k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam,
                                                            p->scal, p->dense, ld);
         DPV_CHECK_LAUNCH();
-        unsigned int* ticket = reinterpret_cast<unsigned int*>(status + 4);
-        DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
-        DPV_TRY(blocked_factor_solve(p->dense, ld, N, status, p->bsub_part, ticket, st));
-        DPV_TSTART("copy_row", st);
-        k_copy_row<<<grid_for(N, 256), 256, 0, st>>>(p->dense + N * ld, N, dp);
-        DPV_CHECK_LAUNCH();
+        DPV_TRY(dense_factor_solve(p->dense, ld, N, status, dp, p->bsub_part, st));
     }
     return back_substitute(p, lam, dp, dd, st);
 }
@@ -573,15 +361,9 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
 
 int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* status,
                        double* work, cudaStream_t st) {
-    // a: augmented (n+1) x lda buffer with the rhs already in row n
-    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + 4);
+    // a: augmented (n+1) x lda buffer with the rhs already in row n; x -> b
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
-    DPV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
-    DPV_TRY(blocked_factor_solve(a, lda, n, status, work, ticket, st));
-    DPV_TSTART("copy_row", st);
-    k_copy_row<<<grid_for(n, 256), 256, 0, st>>>(a + n * lda, n, b);
-    DPV_CHECK_LAUNCH();
-    return DPV_OK;
+    return dense_factor_solve(a, lda, n, status, b, work, st);
 }
 
 int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
