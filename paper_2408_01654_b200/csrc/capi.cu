@@ -595,10 +595,19 @@ int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev,
     cudaStream_t st = as_stream(stream);
     // augmented copy: rows 0..n-1 = a, row n = b
     const int64_t ld = ((n + 1 + 7) / 8) * 8;
-    double* aug = nullptr;
-    double* work = nullptr;
-    DPV_CUDA(cudaMallocAsync(&aug, sizeof(double) * (n + 1) * ld, st));
-    DPV_CUDA(cudaMallocAsync(&work, sizeof(double) * cholesky_work_doubles(n), st));
+    // workspace kept across calls (grown on demand), as the problem handle does
+    static double* aug = nullptr;
+    static double* work = nullptr;
+    static int64_t cap_n = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (n > cap_n) {
+        if (aug) DPV_CUDA(cudaFree(aug));
+        if (work) DPV_CUDA(cudaFree(work));
+        DPV_CUDA(cudaMalloc(&aug, sizeof(double) * (n + 1) * ld));
+        DPV_CUDA(cudaMalloc(&work, sizeof(double) * cholesky_work_doubles(n)));
+        cap_n = n;
+    }
     DPV_CUDA(cudaMemsetAsync(aug, 0, sizeof(double) * (n + 1) * ld, st));
     DPV_CUDA(cudaMemcpy2DAsync(aug, ld * sizeof(double), a, n * sizeof(double), n * sizeof(double),
                                n, cudaMemcpyDeviceToDevice, st));
@@ -608,8 +617,6 @@ int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev,
         DPV_CUDA(cudaMemcpy2DAsync(a, n * sizeof(double), aug, ld * sizeof(double),
                                    n * sizeof(double), n, cudaMemcpyDeviceToDevice, st));
     }
-    cudaFreeAsync(aug, st);
-    cudaFreeAsync(work, st);
     return s;
 }
 

@@ -17,6 +17,7 @@
 //    grid barrier per panel, using the diagonal-block inverses.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "problem.cuh"
@@ -47,6 +48,13 @@ __global__ void __launch_bounds__(1024) k_potrf_inv(double* __restrict__ A, int6
     for (int i = ty; i < kNB; i += 16)
         D[i * kLdP + tx] = (tx <= i && i < nb) ? A[(c0 + i) * ld + c0 + tx] : 0.0;
     __syncthreads();
+    // T starts as the identity; it becomes the row-unscaled inverse (below)
+    for (int i = ty; i < kNB; i += 16) X[i * kLdP + tx] = (i == tx) ? 1.0 : 0.0;
+    __syncthreads();
+    // Unscaled elimination, one barrier per column.  At step j column j of D
+    // and row j of T are final; threads with tx > j update the trailing D,
+    // threads with tx <= j update T (forward substitution of L X = I):
+    //   D[i][k] -= D[i][j] D[k][j] / d_j,   T[i][c] -= D[i][j] T[j][c] / d_j.
     int bad = -1;
     for (int j = 0; j < nb; ++j) {
         double piv = D[j * kLdP + j];
@@ -54,43 +62,27 @@ __global__ void __launch_bounds__(1024) k_potrf_inv(double* __restrict__ A, int6
             if (bad < 0) bad = j;
             piv = 1.0;
         }
-        if (tx > j && tx < nb) {
-            const double dk = D[tx * kLdP + j] / piv;
+        const double inv = 1.0 / piv;
+        const double f = (tx > j ? D[tx * kLdP + j] : X[j * kLdP + tx]) * inv;
+        double* tgt = tx > j ? D : X;
+        if (tx < nb)
             for (int i = j + 1 + ty; i < nb; i += 16)
-                if (tx <= i) D[i * kLdP + tx] -= D[i * kLdP + j] * dk;
-        }
+                if (tx > j ? tx <= i : true) tgt[i * kLdP + tx] -= D[i * kLdP + j] * f;
         __syncthreads();
     }
-    // scale columns: L[i][k] = D[i][k] / sqrt(d_k); diagonal = sqrt(d_k)
+    // scale: L[i][k] = D[i][k] / sqrt(d_k), diag sqrt(d_k); X[i][c] = T[i][c] / sqrt(d_i)
     if (tid < kNB) {
         const double d = D[tid * kLdP + tid];
         dinv[tid] = (tid < nb && d > 0.0) ? sqrt(d) : 1.0;
     }
     __syncthreads();
-    for (int i = ty; i < nb; i += 16)
+    for (int i = ty; i < nb; i += 16) {
         if (tx < i) D[i * kLdP + tx] /= dinv[tx];
+        X[i * kLdP + tx] = tx <= i ? X[i * kLdP + tx] / dinv[i] : 0.0;
+    }
     __syncthreads();
     if (tid < nb) D[tid * kLdP + tid] = dinv[tid];
     __syncthreads();
-    if (tid < kNB) dinv[tid] = tid < nb ? 1.0 / D[tid * kLdP + tid] : 0.0;
-    __syncthreads();
-    // X = L^-1 by rows: X[i][c] = -dinv[i] * sum_{c<=m<i} L[i][m] X[m][c], X[i][i] = dinv[i]
-    for (int i = 0; i < nb; ++i) {
-        // thread (tx = c, ty = part) partial sums over m, reduced across the 16 parts
-        double s = 0.0;
-        if (tx < i)
-            for (int m = tx + ty; m < i; m += 16) s += D[i * kLdP + m] * X[m * kLdP + tx];
-        // reduce over ty through shared memory (reuse dinv-free scratch in X's unused row)
-        __shared__ double red[16][kNB];
-        red[ty][tx] = s;
-        __syncthreads();
-        if (ty == 0) {
-            double t = 0.0;
-            for (int q = 0; q < 16; ++q) t += red[q][tx];
-            X[i * kLdP + tx] = tx < i ? -dinv[i] * t : (tx == i ? dinv[i] : 0.0);
-        }
-        __syncthreads();
-    }
     for (int i = ty; i < nb; i += 16)
         if (tx <= i) A[(c0 + i) * ld + c0 + tx] = D[i * kLdP + tx];
     double* out = Linv + (c0 / kNB) * kNB * kNB;
@@ -103,7 +95,7 @@ __global__ void __launch_bounds__(1024) k_potrf_inv(double* __restrict__ A, int6
 // trailing update on DMMA
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(c0), "+d"(c1)
         : "d"(a), "d"(b));
@@ -117,35 +109,54 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-// columns [col_lo, col_hi), rows [col_lo, N] (row N = rhs); lower tiles only.
-// Requires ld % 2 == 0 and 16-byte aligned rows (ld multiple of 8).
-__global__ void __launch_bounds__(128) k_syrk(double* __restrict__ A, int64_t ld, int64_t N,
-                                              int64_t c0, int nb, int64_t col_lo,
-                                              int64_t col_hi) {
+// Trailing update C -= L_I L_J^T with K = 64 or 128 (one or two panels):
+// columns [col_lo, col_hi), rows [col_lo, N] (row N = rhs), lower tiles
+// only.  64x64 tile per CTA, 4 warps x 32x32 on DMMA m8n8k4.  The
+// accumulators start as C itself (loaded while the first operand chunk
+// streams in) and the A fragments are negated, so D = (-L_I) L_J^T + C needs
+// no extra registers; K streams through a 2-stage cp.async ring of 32-wide
+// chunks.  ~110 registers and 74 KB of shared memory -> 3 CTAs / SM.
+constexpr int kKC = 32;                 // K chunk
+constexpr int kLdC = kKC + 4;           // = 4 (mod 16) doubles
+constexpr int kStages = 2;
+
+__device__ __forceinline__ void stage_chunk(double* As, double* Bs, const double* __restrict__ A,
+                                            int64_t ld, int64_t N, int64_t row0, int64_t col0,
+                                            int64_t col_hi, int64_t kc, int64_t kend, int tid) {
+    // 64 rows x 32 doubles per operand = 1024 16-byte chunks -> 8 per thread
+    for (int x = tid; x < kT * (kKC / 2); x += 128) {
+        const int r = x >> 4, k = (x & 15) * 2;
+        const int64_t gr = row0 + r, gc = col0 + r;
+        const bool kin = kc + k < kend;
+        double* da = As + r * kLdC + k;
+        double* db = Bs + r * kLdC + k;
+        if (gr <= N && kin) cp_async16(da, A + gr * ld + kc + k);
+        else { da[0] = 0.0; da[1] = 0.0; }
+        if (gc < col_hi && kin) cp_async16(db, A + gc * ld + kc + k);
+        else { db[0] = 0.0; db[1] = 0.0; }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(128, 3) k_syrk(double* __restrict__ A, int64_t ld, int64_t N,
+                                                 int64_t c0, int kvalid, int64_t col_lo,
+                                                 int64_t col_hi) {
     const int ti = blockIdx.y, tj = blockIdx.x;
     if (tj > ti) return;
     const int64_t row0 = col_lo + (int64_t)ti * kT;
     const int64_t col0 = col_lo + (int64_t)tj * kT;
+    const int64_t kend = c0 + kvalid;
     extern __shared__ double sm[];
-    double* As = sm;
-    double* Bs = sm + kT * kLdS;
     const int tid = threadIdx.x;
-    // async staging of the two 64 x nb panel slices (16-byte chunks)
-    for (int x = tid; x < kT * (kNB / 2); x += 128) {
-        const int r = x >> 5, k = (x & 31) * 2;
-        const int64_t gr = row0 + r, gc = col0 + r;
-        double* da = As + r * kLdS + k;
-        double* db = Bs + r * kLdS + k;
-        if (gr <= N && k < nb) cp_async16(da, A + gr * ld + c0 + k);
-        else { da[0] = 0.0; da[1] = 0.0; }
-        if (gc < col_hi && k < nb) cp_async16(db, A + gc * ld + c0 + k);
-        else { db[0] = 0.0; db[1] = 0.0; }
-    }
+    constexpr int NK = K / kKC;
+    double* As[kStages] = {sm, sm + 2 * kT * kLdC};
+    double* Bs[kStages] = {sm + kT * kLdC, sm + 3 * kT * kLdC};
+    stage_chunk(As[0], Bs[0], A, ld, N, row0, col0, col_hi, c0, kend, tid);
     const int warp = tid >> 5, lane = tid & 31;
     const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
     const int fr = lane >> 2, fk = lane & 3;
-    // prefetch this thread's C fragments while the operands stream in
-    double cfrag[4][4][2];
+    double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int64_t gr = row0 + wr + a * 8 + fr;
@@ -154,30 +165,37 @@ __global__ void __launch_bounds__(128) k_syrk(double* __restrict__ A, int64_t ld
             const int64_t gc = col0 + wc + b * 8 + 2 * fk;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t c = gc + h;
-                const bool ok = gr <= N && c < col_hi && (c <= gr || gr == N);
-                cfrag[a][b][h] = ok ? A[gr * ld + c] : 0.0;
+                const int64_t cc = gc + h;
+                const bool ok = gr <= N && cc < col_hi && (cc <= gr || gr == N);
+                acc[a][b][h] = ok ? __ldcg(A + gr * ld + cc) : 0.0;
             }
         }
     }
-    cp_async_wait_all();
-    __syncthreads();
-    double acc[4][4][2];
+#pragma unroll 1
+    for (int c = 0; c < NK; ++c) {
+        if (c + 1 < NK) {
+            stage_chunk(As[(c + 1) & 1], Bs[(c + 1) & 1], A, ld, N, row0, col0, col_hi,
+                        c0 + (c + 1) * kKC, kend, tid);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const double* a_s = As[c & 1];
+        const double* b_s = Bs[c & 1];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+        for (int k = 0; k < kKC; k += 4) {
+            double af[4], bf[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < kNB; k += 4) {
-        double af[4], bf[4];
+            for (int a = 0; a < 4; ++a) af[a] = -a_s[(wr + a * 8 + fr) * kLdC + k + fk];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) af[a] = As[(wr + a * 8 + fr) * kLdS + k + fk];
+            for (int b = 0; b < 4; ++b) bf[b] = b_s[(wc + b * 8 + fr) * kLdC + k + fk];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) bf[b] = Bs[(wc + b * 8 + fr) * kLdS + k + fk];
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        __syncthreads();
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -187,9 +205,9 @@ __global__ void __launch_bounds__(128) k_syrk(double* __restrict__ A, int64_t ld
             const int64_t gc = col0 + wc + b * 8 + 2 * fk;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t c = gc + h;
-                if (gr <= N && c < col_hi && (c <= gr || gr == N))
-                    A[gr * ld + c] = cfrag[a][b][h] - acc[a][b][h];
+                const int64_t cc = gc + h;
+                if (gr <= N && cc < col_hi && (cc <= gr || gr == N))
+                    A[gr * ld + cc] = acc[a][b][h];
             }
         }
     }
@@ -302,6 +320,7 @@ __global__ void __launch_bounds__(256) k_bsub_coop(const double* __restrict__ A,
     }
 }
 
+
 struct Ctx {
     cudaStream_t hi = nullptr, lo = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -315,23 +334,25 @@ Ctx& ctx() {
 
 constexpr size_t kPotrfSmem = sizeof(double) * (2 * kNB * kLdP);
 constexpr size_t kTileSmem = sizeof(double) * 2 * kT * kLdS;
+constexpr size_t kSyrkSmem = sizeof(double) * kStages * 2 * kT * kLdC;
 
-int32_t setup(int64_t np) {
+int32_t setup(int64_t ngroups) {
     Ctx& c = ctx();
     if (!c.hi) {
         int lo_prio = 0, hi_prio = 0;
         DPV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
         DPV_CUDA(cudaStreamCreateWithPriority(&c.hi, cudaStreamNonBlocking, hi_prio));
         DPV_CUDA(cudaStreamCreateWithPriority(&c.lo, cudaStreamNonBlocking, lo_prio));
-        static size_t s1 = 0, s2 = 0, s3 = 0;
+        static size_t s1 = 0, s2 = 0, s3 = 0, s4 = 0;
         DPV_TRY(ensure_smem(k_potrf_inv, kPotrfSmem, s1));
-        DPV_TRY(ensure_smem(k_syrk, kTileSmem, s2));
-        DPV_TRY(ensure_smem(k_trsm, kTileSmem, s3));
+        DPV_TRY(ensure_smem(k_syrk<64>, kSyrkSmem, s2));
+        DPV_TRY(ensure_smem(k_syrk<128>, kSyrkSmem, s3));
+        DPV_TRY(ensure_smem(k_trsm, kTileSmem, s4));
         int per_sm = 0;
         DPV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsub_coop, 256, 0));
         c.coop_blocks = std::max(1, std::min(per_sm, 1) * sm_count());
     }
-    while ((int64_t)c.ev.size() < 2 * np + 4) {
+    while ((int64_t)c.ev.size() < 2 * ngroups + 4) {
         cudaEvent_t e;
         DPV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c.ev.push_back(e);
@@ -339,14 +360,34 @@ int32_t setup(int64_t np) {
     return DPV_OK;
 }
 
-int32_t launch_syrk(double* A, int64_t ld, int64_t N, int64_t c0, int nb, int64_t lo,
+// C[lo:hi cols, rows >= lo] -= L[:, c0:c0+k] L[...]^T, k <= 128 valid columns
+int32_t launch_syrk(double* A, int64_t ld, int64_t N, int64_t c0, int k, int64_t lo,
                     int64_t hi, cudaStream_t st) {
-    if (hi <= lo) return DPV_OK;
+    if (hi <= lo || k <= 0) return DPV_OK;
     const int trows = (int)(((N + 1 - lo) + kT - 1) / kT);
     const int tcols = (int)(((hi - lo) + kT - 1) / kT);
     DPV_TSTART("syrk", st);
-    k_syrk<<<dim3(tcols, trows), 128, kTileSmem, st>>>(A, ld, N, c0, nb, lo, hi);
+    if (k <= 64)
+        k_syrk<64><<<dim3(tcols, trows), 128, kSyrkSmem, st>>>(A, ld, N, c0, k, lo, hi);
+    else
+        k_syrk<128><<<dim3(tcols, trows), 128, kSyrkSmem, st>>>(A, ld, N, c0, k, lo, hi);
     DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t factor_panel(double* A, int64_t ld, int64_t N, int64_t p, double* linv,
+                     int32_t* status, cudaStream_t st) {
+    const int64_t c0 = p * kNB;
+    const int nb = (int)std::min<int64_t>(kNB, N - c0);
+    const int64_t below = (N + 1) - (c0 + nb);
+    DPV_TSTART("potrf_inv", st);
+    k_potrf_inv<<<1, 1024, kPotrfSmem, st>>>(A, ld, N, c0, nb, linv, status);
+    DPV_CHECK_LAUNCH();
+    if (below > 0) {
+        DPV_TSTART("trsm", st);
+        k_trsm<<<(int)((below + kT - 1) / kT), 128, kTileSmem, st>>>(A, ld, N, c0, nb, linv);
+        DPV_CHECK_LAUNCH();
+    }
     return DPV_OK;
 }
 
@@ -357,50 +398,51 @@ int64_t dense_workspace_doubles(int64_t N) {
     return np * kNB * kNB + 2 * 160 * kNB + 64;
 }
 
-// Factor + solve on the augmented matrix; x (N) receives S^-1 b.
+// Factor + solve on the augmented matrix; x (N) receives S^-1 b.  Panels of
+// 64 columns are grouped in pairs so the trailing update runs with K = 128.
 int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* x,
                            double* ws, cudaStream_t st) {
     DPV_ARG(ld % 8 == 0 && ld >= N + 1, "dense ld must be a multiple of 8 and > N");
+    constexpr int kGroup = 2 * kNB;
     const int64_t np = (N + kNB - 1) / kNB;
-    DPV_TRY(setup(np));
+    const int64_t ng = (N + kGroup - 1) / kGroup;
+    DPV_TRY(setup(ng));
     Ctx& c = ctx();
     double* linv = ws;
     double* part = ws + np * kNB * kNB;
     cudaEvent_t* evT = c.ev.data();
-    cudaEvent_t* evR = c.ev.data() + np;
-    cudaEvent_t fork = c.ev[2 * np], join_hi = c.ev[2 * np + 1];
-    // fork both streams after everything already queued on the caller's stream
+    cudaEvent_t* evR = c.ev.data() + ng;
+    cudaEvent_t fork = c.ev[2 * ng], join_hi = c.ev[2 * ng + 1];
+    static const bool lookahead = !getenv("DPV_CHOL_LOOKAHEAD") ||
+                                  atoi(getenv("DPV_CHOL_LOOKAHEAD")) != 0;
+    cudaStream_t hi = lookahead ? c.hi : st, lo = lookahead ? c.lo : st;
     DPV_CUDA(cudaEventRecord(fork, st));
-    DPV_CUDA(cudaStreamWaitEvent(c.hi, fork, 0));
-    DPV_CUDA(cudaStreamWaitEvent(c.lo, fork, 0));
-    for (int64_t p = 0; p < np; ++p) {
-        const int64_t c0 = p * kNB;
-        const int nb = (int)std::min<int64_t>(kNB, N - c0);
-        const int64_t below = (N + 1) - (c0 + nb);
-        DPV_TSTART("potrf_inv", c.hi);
-        k_potrf_inv<<<1, 1024, kPotrfSmem, c.hi>>>(A, ld, N, c0, nb, linv, status);
-        DPV_CHECK_LAUNCH();
-        if (below > 0) {
-            DPV_TSTART("trsm", c.hi);
-            k_trsm<<<(int)((below + kT - 1) / kT), 128, kTileSmem, c.hi>>>(A, ld, N, c0, nb,
-                                                                          linv);
-            DPV_CHECK_LAUNCH();
+    DPV_CUDA(cudaStreamWaitEvent(hi, fork, 0));
+    DPV_CUDA(cudaStreamWaitEvent(lo, fork, 0));
+    for (int64_t g = 0; g < ng; ++g) {
+        const int64_t g0 = g * kGroup;                       // group columns [g0, g1)
+        const int64_t g1 = std::min<int64_t>(g0 + kGroup, N);
+        const int64_t p0 = g0 / kNB;
+        // first panel, intra-group update of the second panel, second panel
+        DPV_TRY(factor_panel(A, ld, N, p0, linv, status, hi));
+        if (g0 + kNB < g1) {
+            DPV_TRY(launch_syrk(A, ld, N, g0, kNB, g0 + kNB, g1, hi));
+            DPV_TRY(factor_panel(A, ld, N, p0 + 1, linv, status, hi));
         }
-        DPV_CUDA(cudaEventRecord(evT[p], c.hi));
-        const int64_t s1 = c0 + nb;                       // next panel's first column
-        const int64_t s2 = std::min<int64_t>(s1 + kNB, N);
-        // look-ahead: the next panel's columns, after the previous rest-update
-        if (p > 0) DPV_CUDA(cudaStreamWaitEvent(c.hi, evR[p - 1], 0));
-        DPV_TRY(launch_syrk(A, ld, N, c0, nb, s1, s2, c.hi));
+        DPV_CUDA(cudaEventRecord(evT[g], hi));
+        const int k = (int)(g1 - g0);
+        const int64_t n1 = std::min<int64_t>(g1 + kGroup, N);   // next group's columns
+        // look-ahead: the next group's columns, after the previous rest-update
+        if (g > 0) DPV_CUDA(cudaStreamWaitEvent(hi, evR[g - 1], 0));
+        DPV_TRY(launch_syrk(A, ld, N, g0, k, g1, n1, hi));
         // the rest of the trailing matrix, low priority
-        DPV_CUDA(cudaStreamWaitEvent(c.lo, evT[p], 0));
-        DPV_TRY(launch_syrk(A, ld, N, c0, nb, s2, N, c.lo));
-        DPV_CUDA(cudaEventRecord(evR[p], c.lo));
+        DPV_CUDA(cudaStreamWaitEvent(lo, evT[g], 0));
+        DPV_TRY(launch_syrk(A, ld, N, g0, k, n1, N, lo));
+        DPV_CUDA(cudaEventRecord(evR[g], lo));
     }
-    // join
-    DPV_CUDA(cudaEventRecord(join_hi, c.hi));
+    DPV_CUDA(cudaEventRecord(join_hi, hi));
     DPV_CUDA(cudaStreamWaitEvent(st, join_hi, 0));
-    DPV_CUDA(cudaStreamWaitEvent(st, evR[np - 1], 0));
+    DPV_CUDA(cudaStreamWaitEvent(st, evR[ng - 1], 0));
     const int G = std::min<int>(c.coop_blocks, 160);
     void* args[] = {&A, &ld, &N, &linv, &part, &x};
     DPV_TSTART("bsub", st);

@@ -29,13 +29,16 @@ def main():
     for r in range(reps + 1):
         a = a0.clone()
         b = b0.clone()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        e0.record()
         _lib.check(lib.dpv_cholesky_solve(_lib.ptr(a), _lib.ptr(b), N, _lib.ptr(status),
                                           _lib.stream_ptr()), "solve")
+        e1.record()
         torch.cuda.synchronize()
         if r:
-            times.append(time.perf_counter() - t0)
+            times.append(e0.elapsed_time(e1) * 1e-3)
     res = (a0 @ b - b0).abs().max().item() / b0.abs().max().item()
     # per-kernel split (note: dpv_cholesky_solve also copies the matrix)
     _lib.timing_enable(True)
