@@ -144,12 +144,18 @@ def build_workload(args, torch):
     gen_s = time.perf_counter() - t0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    prob = ba.BAProblem(graph, free)
-    prob._ensure()
+    sharded = int(os.environ.get("WORLD_SIZE", "1")) > 1
+    if sharded:
+        from paper_2408_01654_b200 import dist as pdist
+        prob = pdist.ShardedProblem(graph, free)
+        info = prob.info
+    else:
+        prob = ba.BAProblem(graph, free)
+        prob._ensure()
+        info = prob.info()
     torch.cuda.synchronize()
     build_ms = (time.perf_counter() - t0) * 1e3
-    info = prob.info()
-    E = int(info.n_edges)
+    E = int(prob.n_edges_total) if sharded else int(info.n_edges)
     q, t, d = prob.device_state()
     # correlation inputs: features of the frames the corr edges read
     csel = corr_edge_selection(graph, prob, args.window, torch)
@@ -169,6 +175,7 @@ def build_workload(args, torch):
     gmap = (torch.randn((graph.n_patches, 9, C), generator=gen, device="cuda")
             / math.sqrt(C)).to(fdt)
     work = dict(graph=graph, scene=scene, prob=prob, info=info, E=E, q=q, t=t, d=d, free=free,
+                sharded=sharded, E_local=int(info.n_edges),
                 csel=csel, ii=c_gid.to(torch.int32), jj=jj.to(torch.int32), pyr=pyr, gmap=gmap,
                 n_feat_frames=len(frames), H0=H0, W0=W0, C=C, gen_s=gen_s, build_ms=build_ms)
     return work
@@ -217,12 +224,17 @@ class Stepper:
         self.torch.index_select(self.coords_all, 0, w["csel"], out=self.coords)
         corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
         L.check(lib.dpv_assemble(self.h, P(q), P(t), P(d), s), "assemble")
+        if w["sharded"]:
+            w["prob"].allreduce_system()      # NCCL: reduced pose system
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
                 "solve")
         L.check(lib.dpv_apply_step(self.h, P(q), P(t), P(d), P(self.dp), P(self.dd), P(self.q2),
                                    P(self.t2), P(self.d2), s), "apply_step")
-        L.check(lib.dpv_objective(self.h, P(self.q2), P(self.t2), P(self.d2), P(self.obj), s),
-                "objective")
+        if w["sharded"]:
+            w["prob"].objective(self.q2, self.t2, self.d2, self.obj)   # + all-reduce(sum)
+        else:
+            L.check(lib.dpv_objective(self.h, P(self.q2), P(self.t2), P(self.d2), P(self.obj),
+                                      s), "objective")
 
 
 def time_steps(fn, k, torch):
@@ -255,7 +267,7 @@ def cholesky_flops(N, nb=64):
 
 
 def kernel_rooflines(timing, work, steps, hbm_peak):
-    E = work["E"]
+    E = work["E_local"]     # this rank's edges (= E at N = 1)
     info = work["info"]
     P = int(info.n_depths)
     n = int(info.n_free)
@@ -354,10 +366,14 @@ def run_ours(args):
     import torch
     from paper_2408_01654_b200 import _lib, ba
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if world > 1:
-        from paper_2408_01654_b200 import dist
-        return dist.bench_sharded(args)
-    torch.cuda.set_device(0)
+        import torch.distributed as tdist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK))
     work = build_workload(args, torch)
@@ -365,11 +381,18 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         st.step()
     torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
     launches0 = _lib.lib().dpv_launch_count()
-    with ClockSampler() as clk:
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         ms = time_steps(st.step, args.steps, torch)
     launches = _lib.lib().dpv_launch_count() - launches0
     ms_per_step = ms / args.steps
+    if world > 1:
+        tdist.barrier()
+        mt = torch.tensor([ms_per_step], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(mt, op=tdist.ReduceOp.MAX)        # max over ranks
+        ms_per_step = float(mt.item())
     value = work["E"] / (ms_per_step * 1e-3)
     # per-kernel CUDA-event timing pass (separate, so the headline has no event overhead)
     _lib.timing_enable(True)
@@ -389,18 +412,29 @@ def run_ours(args):
 
     # e2e through the C-ABI from pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         e2e = run_e2e(work, st, args, torch)
 
     # global loop-closure BA (loop.close: new BAProblem + solve(8 iters, 1e-9))
     glob = None
-    if not args.no_global:
+    if not args.no_global and world == 1:
         glob = run_global(work, args, torch)
+    elif not args.no_global:
+        t0 = time.perf_counter()
+        rep, *_ = work["prob"].solve(max_iterations=args.lm_iters, tolerance=1e-9)
+        torch.cuda.synchronize()
+        glob = {"ms": (time.perf_counter() - t0) * 1e3, "iterations": rep["iterations"],
+                "lm_attempts": rep["attempts"], "final_objective": rep["final_objective"],
+                "includes": "native LM over the sharded system (index prebuilt)"}
 
-    cpu = None if args.no_cpu else cpu_sample(work)
+    cpu = None if (args.no_cpu or world > 1) else cpu_sample(work)
+    if world > 1:
+        tdist.destroy_process_group()
+        if rank != 0:
+            return None
     line = {
         "metric": "patch-edges/sec for corr lookup + Gauss-Newton BA step; global loop-closure BA ms",
-        "value": value, "unit": "patch-edges/s", "n_gpus": 1, "steps": args.steps,
+        "value": value, "unit": "patch-edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bit-exactly; random features)",
@@ -412,7 +446,9 @@ def run_ours(args):
                    "W_blocks": int(work["info"].n_keys), "pairs": int(work["info"].n_pairs),
                    "corr_levels": 2, "corr_channels": work["C"], "corr_dtype": args.feat_dtype,
                    "feature_frames": work["n_feat_frames"],
-                   "lm_attempt_per_step": 1, "parallelism": "single GPU",
+                   "lm_attempt_per_step": 1,
+                   "parallelism": (f"edge-shard x{world} by depth row, NCCL all-reduce of the "
+                                   "reduced pose system" if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (targets 0.72 GB, dense S 1.15 GB)"},
         "gpu_launches": int(launches),
         "roofline": roof,

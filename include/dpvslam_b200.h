@@ -111,6 +111,18 @@ typedef struct dpv_problem_info {
 int32_t dpv_problem_create(const dpv_graph* graph, int32_t first_free, int32_t last_free,
                            const int64_t* edge_indices, int64_t n_edge_indices,
                            void* stream, dpv_problem** out);
+/* Same, for one shard of an edge-partitioned global BA: extra_keys (device
+ * int64, folded a*n+b) are merged into the shard's block pattern so every
+ * shard's pose/Schur blocks line up with the global union_keys (the
+ * all-reduce of SURVEY 8(e)). */
+int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_t last_free,
+                              const int64_t* edge_indices, int64_t n_edge_indices,
+                              const int64_t* extra_keys, int64_t n_extra_keys, void* stream,
+                              dpv_problem** out);
+/* Override the gauge (scale_degenerate, first touched fixed frame) with the
+ * global problem's values (a shard sees only part of the touched frames). */
+int32_t dpv_problem_set_gauge(dpv_problem* prob, int32_t scale_degenerate,
+                              int32_t touched_fixed0);
 int32_t dpv_problem_destroy(dpv_problem* prob);
 int32_t dpv_problem_get_info(const dpv_problem* prob, dpv_problem_info* info);
 

@@ -199,3 +199,6 @@ def timing_collect() -> dict:
           "timing_collect")
     keys = names.value.decode().split("\n")[:n.value]
     return {k: (ms[i], int(cnt[i])) for i, k in enumerate(keys)}
+SIGNATURES["dpv_problem_create_ex"] = (C.c_int32, [C.POINTER(DpvGraph), C.c_int32, C.c_int32, vp,
+                                                   C.c_int64, vp, C.c_int64, vp, C.POINTER(vp)])
+SIGNATURES["dpv_problem_set_gauge"] = (C.c_int32, [vp, C.c_int32, C.c_int32])

@@ -306,7 +306,11 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
         const bool act = c > kActiveEps;
         active[r] = act ? 1 : 0;
         cinv0[r] = act ? 1.0 / c : 0.0;
-        if (act) atomicMax(grad_bits, (unsigned long long)__double_as_longlong(fabs(g)));
+        if (act) {
+            const unsigned long long gb = (unsigned long long)__double_as_longlong(fabs(g));
+            atomicMax(grad_bits, gb);
+            atomicMax(grad_bits + 7, gb);   // depth-only part (sharded BA)
+        }
         else atomicAdd(n_inactive, 1ull);
     }
 }

@@ -56,6 +56,19 @@ void timer_push(const char* name, cudaStream_t st, bool start) {
     }
 }
 
+int32_t configure_pool() {
+    static bool done = false;
+    if (done) return DPV_OK;
+    int dev = 0;
+    DPV_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    DPV_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    DPV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done = true;
+    return DPV_OK;
+}
+
 int sm_count() {
     static int cached = 0;
     if (cached == 0) {
@@ -317,18 +330,36 @@ int32_t dpv_reproject_grid(const double* rays, const double* inv_depth, const do
 int32_t dpv_problem_create(const dpv_graph* graph, int32_t first_free, int32_t last_free,
                            const int64_t* edge_indices, int64_t n_edge_indices, void* stream,
                            dpv_problem** out) {
+    return dpv_problem_create_ex(graph, first_free, last_free, edge_indices, n_edge_indices,
+                                 nullptr, 0, stream, out);
+}
+
+int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_t last_free,
+                              const int64_t* edge_indices, int64_t n_edge_indices,
+                              const int64_t* extra_keys, int64_t n_extra_keys, void* stream,
+                              dpv_problem** out) {
     clear_error();
     DPV_ARG(out != nullptr, "out is NULL");
     *out = nullptr;
+    DPV_TRY(configure_pool());
     dpv_problem* p = new (std::nothrow) dpv_problem();
     DPV_ARG(p != nullptr, "allocation failed");
+    p->alloc_stream = as_stream(stream);
     int32_t s = build_problem(graph, first_free, last_free, edge_indices, n_edge_indices,
-                              as_stream(stream), p);
+                              extra_keys, n_extra_keys, as_stream(stream), p);
     if (s != DPV_OK) {
         delete p;
         return s;
     }
     *out = p;
+    return DPV_OK;
+}
+
+int32_t dpv_problem_set_gauge(dpv_problem* prob, int32_t scale_degenerate,
+                              int32_t touched_fixed0) {
+    DPV_ARG(prob, "NULL problem");
+    prob->scale_degenerate = scale_degenerate ? 1 : 0;
+    prob->touched0 = touched_fixed0;
     return DPV_OK;
 }
 

@@ -367,7 +367,8 @@ int32_t frame_rotations(dpv_problem* p, const double* q, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 
 int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int64_t* eidx_in,
-                      int64_t n_eidx, cudaStream_t st, dpv_problem* P) {
+                      int64_t n_eidx, const int64_t* extra_keys, int64_t n_extra,
+                      cudaStream_t st, dpv_problem* P) {
     DPV_ARG(g != nullptr, "graph is NULL");
     DPV_ARG(g->cells > 0 && g->cells <= 64, "cells out of range");
     DPV_ARG(0 <= first && first <= last && last < g->n_frames, "free range out of bounds");
@@ -763,7 +764,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
     {
-        const int64_t tot = NPR + P->n + 3 * P->S;
+        const int64_t tot = NPR + P->n + 3 * P->S + n_extra;
         uint64_t *all, *alls, *uk;
         DPV_TRY(sc.get(&all, tot));
         DPV_TRY(sc.get(&alls, tot));
@@ -778,6 +779,10 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         if (P->S > 0)
             DPV_CUDA(cudaMemcpyAsync(all + NPR + P->n, hk, sizeof(uint64_t) * 3 * P->S,
                                      cudaMemcpyDeviceToDevice, st));
+        // sharded global BA: every shard carries the global block pattern
+        if (n_extra > 0)
+            DPV_CUDA(cudaMemcpyAsync(all + NPR + P->n + 3 * P->S, extra_keys,
+                                     sizeof(uint64_t) * n_extra, cudaMemcpyDeviceToDevice, st));
         DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
             return cub::DeviceRadixSort::SortKeys(t, b, all, alls, (int)tot, 0, 64, st);
         }));

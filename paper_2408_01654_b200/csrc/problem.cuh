@@ -92,7 +92,7 @@ struct dpv_problem {
     double* rhs_pose = nullptr;    // (n, 6)
     double* rhs_schur = nullptr;   // (n, 6)
     double* scal = nullptr;        // [0]=grad bits, [1]=pin flag, [2..4]=pin u, [5]=objective,
-                                   // [6]=unconstrained count, [7] spare
+                                   // [6]=unconstrained count, [7]=depth-only grad bits
     double* obj_part = nullptr;    // (kObjBlocks)
     int64_t* count_buf = nullptr;  // (2) scratch counters
 
@@ -113,12 +113,13 @@ struct dpv_problem {
 
     std::vector<void*> allocs;     // everything above, freed by destroy
     int64_t bytes = 0;
+    cudaStream_t alloc_stream = nullptr;   // stream-ordered pool allocations
 
     template <typename T>
     int32_t alloc(T** p, int64_t count) {
         size_t b = sizeof(T) * (size_t)(count > 0 ? count : 1);
         void* q = nullptr;
-        cudaError_t e = cudaMalloc(&q, b);
+        cudaError_t e = cudaMallocAsync(&q, b, alloc_stream);
         if (e != cudaSuccess) {
             dpv::set_error(std::string("cudaMalloc ") + std::to_string(b) + ": " +
                            cudaGetErrorString(e));
@@ -130,16 +131,20 @@ struct dpv_problem {
         return DPV_OK;
     }
     ~dpv_problem() {
-        for (void* p : allocs) cudaFree(p);
+        // returned to the device pool (release threshold raised: see
+        // dpv::configure_pool), so the next problem reuses the memory
+        for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
         if (lm_host) cudaFreeHost(lm_host);
     }
 };
 
 namespace dpv {
 constexpr int kSegMax = 128;      // edges per segment chunk
+int32_t configure_pool();
 constexpr int kObjBlocks = 1184;  // 148 SMs x 8
 int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int64_t* eidx,
-                      int64_t n_eidx, cudaStream_t st, dpv_problem* P);
+                      int64_t n_eidx, const int64_t* extra_keys, int64_t n_extra,
+                      cudaStream_t st, dpv_problem* P);
 int32_t frame_rotations(dpv_problem* p, const double* q, cudaStream_t st);
 int32_t objective(dpv_problem* p, const double* q, const double* t, const double* d,
                   double* out, cudaStream_t st);
