@@ -1,22 +1,28 @@
-// K4c: dense FP64 Cholesky factor + solve of the damped reduced camera
-// system S(lambda) (ba.py:451-472: scipy cho_factor/cho_solve = LAPACK
-// potrf/potrs), B200 design:
+// K4c: FP64 Cholesky factor + solve of the damped reduced camera system
+// S(lambda) (ba.py:451-487: scipy cho_factor/cho_solve = LAPACK potrf/potrs;
+// block_cholesky.py:48-111 for the block-sparse backend), B200 design:
 //
 //  * augmented (N+1) x ld row-major lower storage, rhs in row N, so the
 //    right-looking factorisation also produces y = L^-1 b;
+//  * a FactorPlan decides which 64x64 tiles are touched: dense (every lower
+//    tile) or sparse = the symbolic tile-level fill of the pose-block pattern
+//    after a symmetric permutation that moves "border" poses (long-range
+//    loop-closure couplings) last, so the rest is banded.  The
+//    same kernels serve both; the sparse plan skips structurally-zero tiles;
 //  * per 64-column panel, on a high-priority stream (the critical path):
 //      potrf_inv: one CTA factors the 64x64 diagonal block in shared memory
 //                 (one barrier per column) and inverts it;
 //      trsm:      L21 = A21 L11^-T as a DMMA product with the inverse;
-//      syrk_next: the next panel's columns of the trailing update;
-//  * the rest of the trailing update A22 -= L21 L21^T on a low-priority
-//    stream (depth-1 look-ahead), on the FP64 tensor cores
-//    (mma.sync.m8n8k4.f64 -> DMMA; tcgen05 has no f64 kind) with cp.async
-//    operand staging and C fragments prefetched into registers;
+//      syrk:      intra-group update of the second panel, then the next
+//                 group's columns;
+//  * the rest of the trailing update on a low-priority stream (look-ahead),
+//    K = 128 (two panels per group) on the FP64 tensor cores
+//    (mma.sync.m8n8k4.f64 -> DMMA; tcgen05 has no f64 kind);
 //  * backward substitution L^T x = y: one cooperative persistent kernel, one
 //    grid barrier per panel, using the diagonal-block inverses.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -25,12 +31,24 @@
 namespace cg = cooperative_groups;
 
 namespace dpv {
+
+
 namespace {
 
 constexpr int kNB = 64;
-constexpr int kT = 64;            // SYRK / TRSM output tile (rows and cols)
+constexpr int kT = 64;            // tile (rows and cols)
 constexpr int kLdS = kNB + 4;     // smem row stride, = 4 (mod 16) doubles
 constexpr int kLdP = kNB + 1;     // potrf smem stride
+
+__device__ __forceinline__ void tile_rows(int t, int t_rhs, int64_t N, int64_t& r0, int& nr) {
+    if (t == t_rhs) {
+        r0 = N;
+        nr = 1;
+    } else {
+        r0 = (int64_t)t * kT;
+        nr = (N - r0) < kT ? (int)(N - r0) : kT;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // diagonal block: factor + invert in one CTA (1024 threads)
@@ -92,11 +110,10 @@ __global__ void __launch_bounds__(1024) k_potrf_inv(double* __restrict__ A, int6
 }
 
 // ---------------------------------------------------------------------------
-// trailing update on DMMA
+// tensor-core helpers
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm(
-        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(c0), "+d"(c1)
         : "d"(a), "d"(b));
 }
@@ -105,34 +122,28 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
 
-// Trailing update C -= L_I L_J^T with K = 64 or 128 (one or two panels):
-// columns [col_lo, col_hi), rows [col_lo, N] (row N = rhs), lower tiles
-// only.  64x64 tile per CTA, 4 warps x 32x32 on DMMA m8n8k4.  The
-// accumulators start as C itself (loaded while the first operand chunk
-// streams in) and the A fragments are negated, so D = (-L_I) L_J^T + C needs
-// no extra registers; K streams through a 2-stage cp.async ring of 32-wide
-// chunks.  ~110 registers and 74 KB of shared memory -> 3 CTAs / SM.
-constexpr int kKC = 32;                 // K chunk
+// ---------------------------------------------------------------------------
+// Trailing update C -= L_I L_J^T, K = 64 or 128 (one or two panels), over an
+// explicit list of 64x64 output tiles (row tile, col tile).  4 warps x 32x32
+// on DMMA m8n8k4.  Accumulators start as C (loaded while the first operand
+// chunk streams in) and the A fragments are negated, so D = (-L_I) L_J^T + C;
+// K streams through a 2-stage cp.async ring of 32-wide chunks.
+constexpr int kKC = 32;
 constexpr int kLdC = kKC + 4;           // = 4 (mod 16) doubles
 constexpr int kStages = 2;
 
 __device__ __forceinline__ void stage_chunk(double* As, double* Bs, const double* __restrict__ A,
-                                            int64_t ld, int64_t N, int64_t row0, int64_t col0,
-                                            int64_t col_hi, int64_t kc, int64_t kend, int tid) {
-    // 64 rows x 32 doubles per operand = 1024 16-byte chunks -> 8 per thread
+                                            int64_t ld, int64_t r0, int nr, int64_t c0t, int nc,
+                                            int64_t kc, int64_t kend, int tid) {
     for (int x = tid; x < kT * (kKC / 2); x += 128) {
         const int r = x >> 4, k = (x & 15) * 2;
-        const int64_t gr = row0 + r, gc = col0 + r;
         const bool kin = kc + k < kend;
         double* da = As + r * kLdC + k;
         double* db = Bs + r * kLdC + k;
-        if (gr <= N && kin) cp_async16(da, A + gr * ld + kc + k);
+        if (r < nr && kin) cp_async16(da, A + (r0 + r) * ld + kc + k);
         else { da[0] = 0.0; da[1] = 0.0; }
-        if (gc < col_hi && kin) cp_async16(db, A + gc * ld + kc + k);
+        if (r < nc && kin) cp_async16(db, A + (c0t + r) * ld + kc + k);
         else { db[0] = 0.0; db[1] = 0.0; }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -140,41 +151,43 @@ __device__ __forceinline__ void stage_chunk(double* As, double* Bs, const double
 
 template <int K>
 __global__ void __launch_bounds__(128, 3) k_syrk(double* __restrict__ A, int64_t ld, int64_t N,
-                                                 int64_t c0, int kvalid, int64_t col_lo,
-                                                 int64_t col_hi) {
-    const int ti = blockIdx.y, tj = blockIdx.x;
-    if (tj > ti) return;
-    const int64_t row0 = col_lo + (int64_t)ti * kT;
-    const int64_t col0 = col_lo + (int64_t)tj * kT;
+                                                 int64_t c0, int kvalid,
+                                                 const int2* __restrict__ pairs, int t_rhs) {
+    const int2 tp = pairs[blockIdx.x];
+    int64_t row0, col0;
+    int nr, nc;
+    tile_rows(tp.x, t_rhs, N, row0, nr);
+    tile_rows(tp.y, t_rhs, N, col0, nc);
+    const bool diag = tp.x == tp.y;
     const int64_t kend = c0 + kvalid;
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
     constexpr int NK = K / kKC;
     double* As[kStages] = {sm, sm + 2 * kT * kLdC};
     double* Bs[kStages] = {sm + kT * kLdC, sm + 3 * kT * kLdC};
-    stage_chunk(As[0], Bs[0], A, ld, N, row0, col0, col_hi, c0, kend, tid);
+    stage_chunk(As[0], Bs[0], A, ld, row0, nr, col0, nc, c0, kend, tid);
     const int warp = tid >> 5, lane = tid & 31;
     const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
     const int fr = lane >> 2, fk = lane & 3;
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const int64_t gr = row0 + wr + a * 8 + fr;
+        const int r = wr + a * 8 + fr;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int64_t gc = col0 + wc + b * 8 + 2 * fk;
+            const int cb = wc + b * 8 + 2 * fk;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t cc = gc + h;
-                const bool ok = gr <= N && cc < col_hi && (cc <= gr || gr == N);
-                acc[a][b][h] = ok ? __ldcg(A + gr * ld + cc) : 0.0;
+                const int c = cb + h;
+                const bool ok = r < nr && c < nc && (!diag || c <= r);
+                acc[a][b][h] = ok ? __ldcg(A + (row0 + r) * ld + col0 + c) : 0.0;
             }
         }
     }
 #pragma unroll 1
     for (int c = 0; c < NK; ++c) {
         if (c + 1 < NK) {
-            stage_chunk(As[(c + 1) & 1], Bs[(c + 1) & 1], A, ld, N, row0, col0, col_hi,
+            stage_chunk(As[(c + 1) & 1], Bs[(c + 1) & 1], A, ld, row0, nr, col0, nc,
                         c0 + (c + 1) * kKC, kend, tid);
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {
@@ -199,40 +212,42 @@ __global__ void __launch_bounds__(128, 3) k_syrk(double* __restrict__ A, int64_t
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const int64_t gr = row0 + wr + a * 8 + fr;
+        const int r = wr + a * 8 + fr;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int64_t gc = col0 + wc + b * 8 + 2 * fk;
+            const int cb = wc + b * 8 + 2 * fk;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t cc = gc + h;
-                if (gr <= N && cc < col_hi && (cc <= gr || gr == N))
-                    A[gr * ld + cc] = acc[a][b][h];
+                const int c = cb + h;
+                if (r < nr && c < nc && (!diag || c <= r))
+                    A[(row0 + r) * ld + col0 + c] = acc[a][b][h];
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// L21 = A21 L11^-T on DMMA: 64 rows per CTA, K = 64, in place
+// L21 = A21 L11^-T on DMMA over the panel's listed row tiles, in place
 
 __global__ void __launch_bounds__(128) k_trsm(double* __restrict__ A, int64_t ld, int64_t N,
-                                              int64_t c0, int nb, const double* __restrict__ Linv) {
+                                              int64_t c0, int nb, const double* __restrict__ Linv,
+                                              const int* __restrict__ rows, int t_rhs) {
     extern __shared__ double sm[];
     double* As = sm;
     double* Bs = sm + kT * kLdS;
-    const int64_t row0 = c0 + nb + (int64_t)blockIdx.x * kT;
+    int64_t row0;
+    int nr;
+    tile_rows(rows[blockIdx.x], t_rhs, N, row0, nr);
     const double* Li = Linv + (c0 / kNB) * kNB * kNB;
     const int tid = threadIdx.x;
     for (int x = tid; x < kT * (kNB / 2); x += 128) {
         const int r = x >> 5, k = (x & 31) * 2;
-        const int64_t gr = row0 + r;
         double* da = As + r * kLdS + k;
-        if (gr <= N && k < nb) cp_async16(da, A + gr * ld + c0 + k);
+        if (r < nr && k < nb) cp_async16(da, A + (row0 + r) * ld + c0 + k);
         else { da[0] = 0.0; da[1] = 0.0; }
         cp_async16(Bs + r * kLdS + k, Li + r * kNB + k);   // Bs[n][k] = Linv[n][k]
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     const int warp = tid >> 5, lane = tid & 31;
     const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
@@ -256,14 +271,14 @@ __global__ void __launch_bounds__(128) k_trsm(double* __restrict__ A, int64_t ld
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const int64_t gr = row0 + wr + a * 8 + fr;
-        if (gr > N) continue;
+        const int r = wr + a * 8 + fr;
+        if (r >= nr) continue;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int c = wc + b * 8 + 2 * fk;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-                if (c + h < nb) A[gr * ld + c0 + c + h] = acc[a][b][h];
+                if (c + h < nb) A[(row0 + r) * ld + c0 + c + h] = acc[a][b][h];
         }
     }
 }
@@ -320,7 +335,6 @@ __global__ void __launch_bounds__(256) k_bsub_coop(const double* __restrict__ A,
     }
 }
 
-
 struct Ctx {
     cudaStream_t hi = nullptr, lo = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -360,32 +374,30 @@ int32_t setup(int64_t ngroups) {
     return DPV_OK;
 }
 
-// C[lo:hi cols, rows >= lo] -= L[:, c0:c0+k] L[...]^T, k <= 128 valid columns
-int32_t launch_syrk(double* A, int64_t ld, int64_t N, int64_t c0, int k, int64_t lo,
-                    int64_t hi, cudaStream_t st) {
-    if (hi <= lo || k <= 0) return DPV_OK;
-    const int trows = (int)(((N + 1 - lo) + kT - 1) / kT);
-    const int tcols = (int)(((hi - lo) + kT - 1) / kT);
+int32_t launch_syrk(double* A, int64_t ld, int64_t N, int64_t c0, int k, const int2* pairs,
+                    int count, int t_rhs, cudaStream_t st) {
+    if (count <= 0 || k <= 0) return DPV_OK;
     DPV_TSTART("syrk", st);
     if (k <= 64)
-        k_syrk<64><<<dim3(tcols, trows), 128, kSyrkSmem, st>>>(A, ld, N, c0, k, lo, hi);
+        k_syrk<64><<<count, 128, kSyrkSmem, st>>>(A, ld, N, c0, k, pairs, t_rhs);
     else
-        k_syrk<128><<<dim3(tcols, trows), 128, kSyrkSmem, st>>>(A, ld, N, c0, k, lo, hi);
+        k_syrk<128><<<count, 128, kSyrkSmem, st>>>(A, ld, N, c0, k, pairs, t_rhs);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
 }
 
-int32_t factor_panel(double* A, int64_t ld, int64_t N, int64_t p, double* linv,
-                     int32_t* status, cudaStream_t st) {
-    const int64_t c0 = p * kNB;
+int32_t factor_panel(double* A, int64_t ld, int64_t N, int p, const FactorPlan& pl,
+                     double* linv, int32_t* status, cudaStream_t st) {
+    const int64_t c0 = (int64_t)p * kNB;
     const int nb = (int)std::min<int64_t>(kNB, N - c0);
-    const int64_t below = (N + 1) - (c0 + nb);
     DPV_TSTART("potrf_inv", st);
     k_potrf_inv<<<1, 1024, kPotrfSmem, st>>>(A, ld, N, c0, nb, linv, status);
     DPV_CHECK_LAUNCH();
-    if (below > 0) {
+    const int cnt = pl.rows_off[p + 1] - pl.rows_off[p];
+    if (cnt > 0) {
         DPV_TSTART("trsm", st);
-        k_trsm<<<(int)((below + kT - 1) / kT), 128, kTileSmem, st>>>(A, ld, N, c0, nb, linv);
+        k_trsm<<<cnt, 128, kTileSmem, st>>>(A, ld, N, c0, nb, linv, pl.d_rows + pl.rows_off[p],
+                                            pl.T);
         DPV_CHECK_LAUNCH();
     }
     return DPV_OK;
@@ -393,23 +405,112 @@ int32_t factor_panel(double* A, int64_t ld, int64_t N, int64_t p, double* linv,
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// plan construction (host): symbolic tile-level fill of the lower pattern
+
+int32_t build_factor_plan(int64_t N, const std::vector<char>* tile_pattern, FactorPlan& pl) {
+    const int T = (int)((N + kT - 1) / kT);
+    pl.N = N;
+    pl.T = T;
+    pl.dense = tile_pattern == nullptr;
+    std::vector<std::vector<char>> pat(T, std::vector<char>(T, 0));
+    for (int i = 0; i < T; ++i)
+        for (int j = 0; j <= i; ++j)
+            pat[i][j] = pl.dense ? 1 : (*tile_pattern)[(size_t)i * T + j];
+    for (int i = 0; i < T; ++i) pat[i][i] = 1;
+    // symbolic right-looking fill (block_cholesky.py:93-105 at tile granularity)
+    std::vector<std::vector<int>> rows(T);
+    for (int j = 0; j < T; ++j) {
+        for (int i = j + 1; i < T; ++i)
+            if (pat[i][j]) rows[j].push_back(i);
+        const auto& r = rows[j];
+        for (size_t a = 0; a < r.size(); ++a)
+            for (size_t b = 0; b <= a; ++b) pat[r[a]][r[b]] = 1;
+    }
+    const int t_rhs = T;      // the rhs row N is a dense extra row tile
+    std::vector<int> flat_rows;
+    pl.rows_off.assign(T + 1, 0);
+    for (int p = 0; p < T; ++p) {
+        pl.rows_off[p] = (int)flat_rows.size();
+        for (int i : rows[p]) flat_rows.push_back(i);
+        flat_rows.push_back(t_rhs);
+    }
+    pl.rows_off[T] = (int)flat_rows.size();
+    const int ng = (T + 1) / 2;
+    pl.ng = ng;
+    std::vector<int2> pairs;
+    pl.intra_off.assign(ng + 1, 0);
+    pl.next_off.assign(ng + 1, 0);
+    pl.rest_off.assign(ng + 1, 0);
+    pl.rest_end.assign(ng + 1, 0);
+    double flops = 0.0;
+    for (int g = 0; g < ng; ++g) {
+        const int p0 = 2 * g, p1 = 2 * g + 1;
+        pl.intra_off[g] = (int)pairs.size();
+        if (p1 < T) {
+            for (int i : rows[p0])
+                if (i >= p1) pairs.push_back(make_int2(i, p1));
+            pairs.push_back(make_int2(t_rhs, p1));
+            flops += 2.0 * 64 * 64 * 64 * (rows[p0].size() + 1);
+        }
+        // row tiles of the group below it
+        std::vector<int> rg;
+        for (int p : {p0, p1}) {
+            if (p >= T) continue;
+            for (int i : rows[p])
+                if (i > p1) rg.push_back(i);
+        }
+        std::sort(rg.begin(), rg.end());
+        rg.erase(std::unique(rg.begin(), rg.end()), rg.end());
+        const int kk = (p1 < T) ? 128 : 64;
+        pl.next_off[g] = (int)pairs.size();
+        for (int ci : rg) {
+            if (ci > p1 + 2) break;
+            for (int ri : rg)
+                if (ri >= ci) pairs.push_back(make_int2(ri, ci));
+            pairs.push_back(make_int2(t_rhs, ci));
+        }
+        pl.rest_off[g] = (int)pairs.size();
+        for (int ci : rg) {
+            if (ci <= p1 + 2) continue;
+            for (int ri : rg)
+                if (ri >= ci) pairs.push_back(make_int2(ri, ci));
+            pairs.push_back(make_int2(t_rhs, ci));
+        }
+        pl.rest_end[g] = (int)pairs.size();
+        const double ntile = (double)(pl.rest_end[g] - pl.next_off[g]);
+        flops += 2.0 * 64 * 64 * kk * ntile;
+    }
+    pl.pair_count = (int64_t)pairs.size();
+    pl.syrk_flops = flops;
+    if (pl.d_rows) cudaFree(pl.d_rows);
+    if (pl.d_pairs) cudaFree(pl.d_pairs);
+    DPV_CUDA(cudaMalloc(&pl.d_rows, sizeof(int) * std::max<size_t>(1, flat_rows.size())));
+    DPV_CUDA(cudaMalloc(&pl.d_pairs, sizeof(int2) * std::max<size_t>(1, pairs.size())));
+    DPV_CUDA(cudaMemcpy(pl.d_rows, flat_rows.data(), sizeof(int) * flat_rows.size(),
+                        cudaMemcpyHostToDevice));
+    DPV_CUDA(cudaMemcpy(pl.d_pairs, pairs.data(), sizeof(int2) * pairs.size(),
+                        cudaMemcpyHostToDevice));
+    return DPV_OK;
+}
+
 int64_t dense_workspace_doubles(int64_t N) {
     const int64_t np = (N + kNB - 1) / kNB;
     return np * kNB * kNB + 2 * 160 * kNB + 64;
 }
 
-// Factor + solve on the augmented matrix; x (N) receives S^-1 b.  Panels of
-// 64 columns are grouped in pairs so the trailing update runs with K = 128.
+// Factor + solve on the augmented matrix following `pl`; x (N) receives
+// S^-1 b (in the plan's permuted order).  Panels of 64 columns are grouped
+// in pairs so the trailing update runs with K = 128.
 int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* x,
-                           double* ws, cudaStream_t st) {
+                           double* ws, const FactorPlan& pl, cudaStream_t st) {
     DPV_ARG(ld % 8 == 0 && ld >= N + 1, "dense ld must be a multiple of 8 and > N");
-    constexpr int kGroup = 2 * kNB;
-    const int64_t np = (N + kNB - 1) / kNB;
-    const int64_t ng = (N + kGroup - 1) / kGroup;
+    DPV_ARG(pl.N == N, "factor plan built for another size");
+    const int T = pl.T, ng = pl.ng;
     DPV_TRY(setup(ng));
     Ctx& c = ctx();
     double* linv = ws;
-    double* part = ws + np * kNB * kNB;
+    double* part = ws + (int64_t)T * kNB * kNB;
     cudaEvent_t* evT = c.ev.data();
     cudaEvent_t* evR = c.ev.data() + ng;
     cudaEvent_t fork = c.ev[2 * ng], join_hi = c.ev[2 * ng + 1];
@@ -419,25 +520,24 @@ int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, do
     DPV_CUDA(cudaEventRecord(fork, st));
     DPV_CUDA(cudaStreamWaitEvent(hi, fork, 0));
     DPV_CUDA(cudaStreamWaitEvent(lo, fork, 0));
-    for (int64_t g = 0; g < ng; ++g) {
-        const int64_t g0 = g * kGroup;                       // group columns [g0, g1)
-        const int64_t g1 = std::min<int64_t>(g0 + kGroup, N);
-        const int64_t p0 = g0 / kNB;
-        // first panel, intra-group update of the second panel, second panel
-        DPV_TRY(factor_panel(A, ld, N, p0, linv, status, hi));
-        if (g0 + kNB < g1) {
-            DPV_TRY(launch_syrk(A, ld, N, g0, kNB, g0 + kNB, g1, hi));
-            DPV_TRY(factor_panel(A, ld, N, p0 + 1, linv, status, hi));
+    for (int g = 0; g < ng; ++g) {
+        const int p0 = 2 * g, p1 = 2 * g + 1;
+        const int64_t g0 = (int64_t)p0 * kNB;
+        const int64_t g1 = std::min<int64_t>(g0 + 2 * kNB, N);
+        DPV_TRY(factor_panel(A, ld, N, p0, pl, linv, status, hi));
+        if (p1 < T) {
+            DPV_TRY(launch_syrk(A, ld, N, g0, kNB, pl.d_pairs + pl.intra_off[g],
+                                pl.next_off[g] - pl.intra_off[g], T, hi));
+            DPV_TRY(factor_panel(A, ld, N, p1, pl, linv, status, hi));
         }
         DPV_CUDA(cudaEventRecord(evT[g], hi));
         const int k = (int)(g1 - g0);
-        const int64_t n1 = std::min<int64_t>(g1 + kGroup, N);   // next group's columns
-        // look-ahead: the next group's columns, after the previous rest-update
         if (g > 0) DPV_CUDA(cudaStreamWaitEvent(hi, evR[g - 1], 0));
-        DPV_TRY(launch_syrk(A, ld, N, g0, k, g1, n1, hi));
-        // the rest of the trailing matrix, low priority
+        DPV_TRY(launch_syrk(A, ld, N, g0, k, pl.d_pairs + pl.next_off[g],
+                            pl.rest_off[g] - pl.next_off[g], T, hi));
         DPV_CUDA(cudaStreamWaitEvent(lo, evT[g], 0));
-        DPV_TRY(launch_syrk(A, ld, N, g0, k, n1, N, lo));
+        DPV_TRY(launch_syrk(A, ld, N, g0, k, pl.d_pairs + pl.rest_off[g],
+                            pl.rest_end[g] - pl.rest_off[g], T, lo));
         DPV_CUDA(cudaEventRecord(evR[g], lo));
     }
     DPV_CUDA(cudaEventRecord(join_hi, hi));

@@ -6,6 +6,27 @@
 
 #include "common.cuh"
 
+namespace dpv {
+// Which 64x64 tiles the Cholesky touches (dense or symbolic tile fill); see cholesky.cu.
+struct FactorPlan {
+    int64_t N = -1;
+    int T = 0;                        // 64-row tiles over [0, N); tile T = the rhs row N
+    int ng = 0;                       // panel groups (2 panels each)
+    bool dense = true;
+    int* d_rows = nullptr;            // trsm row tiles, per panel
+    std::vector<int> rows_off;        // T + 1
+    int2* d_pairs = nullptr;          // syrk (row tile, col tile), per group: intra|next|rest
+    std::vector<int> intra_off, next_off, rest_off, rest_end;
+    int64_t pair_count = 0;
+    double syrk_flops = 0.0;          // algorithmic flops of the planned updates
+    ~FactorPlan() {
+        if (d_rows) cudaFree(d_rows);
+        if (d_pairs) cudaFree(d_pairs);
+    }
+};
+int32_t build_factor_plan(int64_t N, const std::vector<char>* tile_pattern, FactorPlan& pl);
+}  // namespace dpv
+
 struct dpv_problem {
     // ---- sizes -------------------------------------------------------------
     int32_t F = 0;      // graph frames
@@ -101,7 +122,9 @@ struct dpv_problem {
     double* cinv = nullptr;        // (P)
     double* dense = nullptr;       // (N+1) x ld lower, lazily allocated
     int64_t dense_ld = 0;
-    double* bsub_part = nullptr;   // back-substitution partials
+    double* bsub_part = nullptr;   // back-substitution partials + diag inverses
+    dpv::FactorPlan* plan = nullptr;  // tile plan of the reduced system (lazily built)
+    int32_t* perm_pos = nullptr;   // (n) pose var -> permuted position in the dense solve
     int32_t* status = nullptr;     // (4) device flags
 
     // ---- LM scratch ------------------------------------------------------------
@@ -135,6 +158,7 @@ struct dpv_problem {
         // dpv::configure_pool), so the next problem reuses the memory
         for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
         if (lm_host) cudaFreeHost(lm_host);
+        delete plan;
     }
 };
 
@@ -169,5 +193,5 @@ int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* st
 int64_t cholesky_work_doubles(int64_t n);
 int64_t dense_workspace_doubles(int64_t N);
 int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, double* x,
-                           double* ws, cudaStream_t st);
+                           double* ws, const FactorPlan& pl, cudaStream_t st);
 }  // namespace dpv

@@ -9,6 +9,10 @@
 // substitution y = L^-1 b for free (the augmented-matrix trick).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
 #include "problem.cuh"
 
 namespace dpv {
@@ -68,38 +72,49 @@ __global__ void k_reduced_vectors(int64_t n6, int64_t P, const double* rhs_pose,
 // ---------------------------------------------------------------------------
 // dense scatter of S(lam) into the lower triangle + rhs row ---------------------
 
+// pose var v sits at position pos[v] of the (possibly permuted) dense system
 __global__ void k_dense_scatter(int64_t W, const int32_t* ka, const int32_t* kb,
                                 const double* pose, const double* schur, double lam, double* A,
-                                int64_t ld) {
+                                int64_t ld, const int32_t* pos) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < W * 36;
          x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = x / 36;
         const int idx = (int)(x % 36);
         const int i = idx / 6, j = idx % 6;
-        const int64_t a = ka[w], b = kb[w];
-        const double v = reduced_entry(pose, schur, w, idx, a == b, lam);
+        const int64_t a = pos[ka[w]], b = pos[kb[w]];
+        const double v = reduced_entry(pose, schur, w, idx, ka[w] == kb[w], lam);
         if (a == b) {
             if (i >= j) A[(6 * a + i) * ld + 6 * a + j] = v;
-        } else {
+        } else if (a < b) {
             // upper block S_ab -> lower mirror S_ba = S_ab^T
             A[(6 * b + j) * ld + 6 * a + i] = v;
+        } else {
+            A[(6 * a + i) * ld + 6 * b + j] = v;
         }
     }
 }
 
 __global__ void k_dense_pin_rhs(int64_t n6, const double* rhs_pose, const double* rhs_schur,
-                                double lam, const double* scal, double* A, int64_t ld) {
+                                double lam, const double* scal, double* A, int64_t ld,
+                                const int32_t* pos) {
     const int64_t N = n6;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
          c += (int64_t)gridDim.x * blockDim.x)
-        A[N * ld + c] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
+        A[N * ld + 6 * (int64_t)pos[c / 6] + c % 6] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
     if (blockIdx.x == 0 && threadIdx.x == 0 && scal[1] != 0.0 && N >= 6) {
+        const int64_t o = 6 * (int64_t)pos[0];   // the pinned block of pose var 0
         double mx = 0.0;
-        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[k * ld + k]));
+        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[(o + k) * ld + o + k]));
         const double mu = 1e6 * fmax(1.0, mx);
         for (int i = 0; i < 3; ++i)
-            for (int j = 0; j <= i; ++j) A[i * ld + j] += mu * scal[2 + i] * scal[2 + j];
+            for (int j = 0; j <= i; ++j) A[(o + i) * ld + o + j] += mu * scal[2 + i] * scal[2 + j];
     }
+}
+
+__global__ void k_unpermute(int64_t n, const int32_t* pos, const double* x, double* dp) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < 6 * n;
+         c += (int64_t)gridDim.x * blockDim.x)
+        dp[c] = x[6 * (int64_t)pos[c / 6] + c % 6];
 }
 
 // ---------------------------------------------------------------------------
@@ -286,7 +301,78 @@ __global__ void k_apply_step(int64_t F, int32_t first, int32_t last, int64_t P, 
 
 int64_t dense_ld(int64_t N) { return ((N + 1 + 7) / 8) * 8; }
 
-int32_t ensure_dense(dpv_problem* p, int64_t N) {
+// Symmetric permutation + tile plan of the reduced camera system (host, once
+// per problem: the pattern = union_keys is state-independent).  Poses with a
+// long-range coupling (a loop-closure block farther than `band` poses from
+// the diagonal) move to the end, so the rest is banded; `band` is chosen to
+// minimise the planned trailing-update work.  With DPV_DENSE_SOLVE=1 every
+// tile is kept (the plain dense factorisation).
+int32_t ensure_plan(dpv_problem* p, int64_t N, cudaStream_t st) {
+    if (p->plan) return DPV_OK;
+    const int64_t n = p->n, W = p->W;
+    std::vector<int32_t> ka(W), kb(W);
+    DPV_CUDA(cudaMemcpyAsync(ka.data(), p->key_a, sizeof(int32_t) * W, cudaMemcpyDeviceToHost, st));
+    DPV_CUDA(cudaMemcpyAsync(kb.data(), p->key_b, sizeof(int32_t) * W, cudaMemcpyDeviceToHost, st));
+    DPV_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> pos(n);
+    for (int64_t v = 0; v < n; ++v) pos[v] = (int32_t)v;
+    const char* env = getenv("DPV_DENSE_SOLVE");
+    const bool dense = env && atoi(env) != 0;
+    auto* plan = new (std::nothrow) FactorPlan();
+    DPV_ARG(plan != nullptr, "allocation failed");
+    if (dense) {
+        int32_t s = build_factor_plan(N, nullptr, *plan);
+        if (s != DPV_OK) { delete plan; return s; }
+    } else {
+        const int T = (int)((N + 63) / 64);
+        double best = -1.0;
+        std::vector<int32_t> best_pos = pos;
+        for (int64_t band : {4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256, 512, 1024}) {
+            if (band >= n && band != 4) break;
+            std::vector<char> border(n, 0);
+            for (int64_t w = 0; w < W; ++w)
+                if (kb[w] - ka[w] > band) border[kb[w]] = 1;
+            std::vector<int32_t> cand(n);
+            int32_t k = 0;
+            for (int64_t v = 0; v < n; ++v)
+                if (!border[v]) cand[v] = k++;
+            const int64_t nb_border = n - k;
+            for (int64_t v = 0; v < n; ++v)
+                if (border[v]) cand[v] = k++;
+            // work estimate: row tiles per panel ~ band tiles + border tiles
+            const double rows = (6.0 * band) / 64.0 + 2.0 + (6.0 * nb_border) / 64.0 + 1.0;
+            const double cost = T * rows * rows;
+            if (best < 0 || cost < best) {
+                best = cost;
+                best_pos = cand;
+            }
+        }
+        pos = best_pos;
+        std::vector<char> pat((size_t)T * T, 0);
+        for (int64_t w = 0; w < W; ++w) {
+            int64_t r = pos[kb[w]], c = pos[ka[w]];
+            if (r < c) std::swap(r, c);
+            for (int64_t tr = (6 * r) / 64; tr <= (6 * r + 5) / 64; ++tr)
+                for (int64_t tc = (6 * c) / 64; tc <= (6 * c + 5) / 64; ++tc)
+                    if (tc <= tr) pat[(size_t)tr * T + tc] = 1;
+        }
+        int32_t s = build_factor_plan(N, &pat, *plan);
+        if (s != DPV_OK) { delete plan; return s; }
+    }
+    if (getenv("DPV_PLAN_DEBUG"))
+        fprintf(stderr, "[dpv] plan N=%lld T=%d dense=%d pairs=%lld syrk_gflop=%.2f\n",
+                (long long)N, plan->T, (int)plan->dense, (long long)plan->pair_count,
+                plan->syrk_flops * 1e-9);
+    DPV_TRY(p->alloc(&p->perm_pos, n));
+    DPV_CUDA(cudaMemcpyAsync(p->perm_pos, pos.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                             st));
+    DPV_CUDA(cudaStreamSynchronize(st));
+    p->plan = plan;
+    return DPV_OK;
+}
+
+int32_t ensure_dense(dpv_problem* p, int64_t N, cudaStream_t st) {
+    DPV_TRY(ensure_plan(p, N, st));
     if (p->dense) return DPV_OK;
     p->dense_ld = dense_ld(N);
     DPV_TRY(p->alloc(&p->dense, (N + 1) * p->dense_ld));
@@ -332,18 +418,23 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
                                              lam, dp, status);
         DPV_CHECK_LAUNCH();
     } else {
-        DPV_TRY(ensure_dense(p, N));
+        DPV_TRY(ensure_dense(p, N, st));
         const int64_t ld = p->dense_ld;
         DPV_CUDA(cudaMemsetAsync(p->dense, 0, sizeof(double) * (N + 1) * ld, st));
         DPV_TSTART("dense_scatter", st);
         k_dense_scatter<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
-            p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld);
+            p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld,
+            p->perm_pos);
         DPV_CHECK_LAUNCH();
         DPV_TSTART("dense_pin_rhs", st);
         k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam,
-                                                           p->scal, p->dense, ld);
+                                                           p->scal, p->dense, ld, p->perm_pos);
         DPV_CHECK_LAUNCH();
-        DPV_TRY(dense_factor_solve(p->dense, ld, N, status, dp, p->bsub_part, st));
+        DPV_TRY(dense_factor_solve(p->dense, ld, N, status, p->red_rhs, p->bsub_part, *p->plan,
+                                   st));
+        DPV_TSTART("unpermute", st);
+        k_unpermute<<<grid_for(N, 256), 256, 0, st>>>(p->n, p->perm_pos, p->red_rhs, dp);
+        DPV_CHECK_LAUNCH();
     }
     return back_substitute(p, lam, dp, dd, st);
 }
@@ -362,8 +453,10 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
 int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* status,
                        double* work, cudaStream_t st) {
     // a: augmented (n+1) x lda buffer with the rhs already in row n; x -> b
+    static FactorPlan dense_plan;   // every tile (the matrix pattern is unknown)
+    if (dense_plan.N != n) DPV_TRY(build_factor_plan(n, nullptr, dense_plan));
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
-    return dense_factor_solve(a, lda, n, status, b, work, st);
+    return dense_factor_solve(a, lda, n, status, b, work, dense_plan, st);
 }
 
 int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
