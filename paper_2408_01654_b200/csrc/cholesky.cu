@@ -18,8 +18,9 @@
 //  * the rest of the trailing update on a low-priority stream (look-ahead),
 //    K = 128 (two panels per group) on the FP64 tensor cores
 //    (mma.sync.m8n8k4.f64 -> DMMA; tcgen05 has no f64 kind);
-//  * backward substitution L^T x = y: one cooperative persistent kernel, one
-//    grid barrier per panel, using the diagonal-block inverses.
+//  * backward substitution L^T x = y using the diagonal-block inverses: one
+//    CTA walking the plan's nonzero tiles (sparse plans), or one cooperative
+//    persistent kernel with a grid barrier per panel (dense plans).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(1024) k_potrf_inv(double* __restrict__ A, int6
             if (bad < 0) bad = j;
             piv = 1.0;
         }
-        const double inv = 1.0 / piv;
+        const double inv = __drcp_rn(piv);
         const double f = (tx > j ? D[tx * kLdP + j] : X[j * kLdP + tx]) * inv;
         double* tgt = tx > j ? D : X;
         if (tx < nb)
@@ -335,6 +336,51 @@ __global__ void __launch_bounds__(256) k_bsub_coop(const double* __restrict__ A,
     }
 }
 
+// Sparse plans: backward substitution by ONE CTA walking the panels from the
+// last, touching only the plan's nonzero row tiles below each diagonal block
+// (no grid barriers; ~7 tiles per panel at cfg3).
+__global__ void __launch_bounds__(1024) k_bsub_seq(const double* __restrict__ A, int64_t ld,
+                                                   int64_t N, const double* __restrict__ Linv,
+                                                   const int* __restrict__ rows,
+                                                   const int* __restrict__ rows_off, int T,
+                                                   double* __restrict__ x) {
+    __shared__ double red[16][kNB];
+    __shared__ double v[kNB];
+    const int tid = threadIdx.x;
+    const int k = tid & 63, rg = tid >> 6;
+    const double* y = A + N * ld;
+    for (int p = T - 1; p >= 0; --p) {
+        const int64_t c0 = (int64_t)p * kNB;
+        const int nb = (N - c0) < kNB ? (int)(N - c0) : kNB;
+        double acc = 0.0;
+        if (k < nb) {
+            for (int e = rows_off[p]; e < rows_off[p + 1]; ++e) {
+                const int t = rows[e];
+                if (t >= T) continue;                 // the rhs pseudo-tile
+                const int64_t r0 = (int64_t)t * kT;
+                const int64_t r1 = (r0 + kT) < N ? r0 + kT : N;
+                for (int64_t r = r0 + rg; r < r1; r += 16) acc += A[r * ld + c0 + k] * x[r];
+            }
+        }
+        red[rg][k] = acc;
+        __syncthreads();
+        if (tid < kNB) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) s += red[q][tid];
+            v[tid] = tid < nb ? y[c0 + tid] - s : 0.0;
+        }
+        __syncthreads();
+        if (tid < nb) {
+            const double* Li = Linv + (int64_t)p * kNB * kNB;
+            double s = 0.0;
+            for (int m = 0; m < nb; ++m) s += Li[m * kNB + tid] * v[m];
+            x[c0 + tid] = s;
+        }
+        __syncthreads();
+    }
+}
+
 struct Ctx {
     cudaStream_t hi = nullptr, lo = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -489,6 +535,10 @@ int32_t build_factor_plan(int64_t N, const std::vector<char>* tile_pattern, Fact
     DPV_CUDA(cudaMalloc(&pl.d_pairs, sizeof(int2) * std::max<size_t>(1, pairs.size())));
     DPV_CUDA(cudaMemcpy(pl.d_rows, flat_rows.data(), sizeof(int) * flat_rows.size(),
                         cudaMemcpyHostToDevice));
+    if (pl.d_rows_off) cudaFree(pl.d_rows_off);
+    DPV_CUDA(cudaMalloc(&pl.d_rows_off, sizeof(int) * pl.rows_off.size()));
+    DPV_CUDA(cudaMemcpy(pl.d_rows_off, pl.rows_off.data(), sizeof(int) * pl.rows_off.size(),
+                        cudaMemcpyHostToDevice));
     DPV_CUDA(cudaMemcpy(pl.d_pairs, pairs.data(), sizeof(int2) * pairs.size(),
                         cudaMemcpyHostToDevice));
     return DPV_OK;
@@ -543,6 +593,12 @@ int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, do
     DPV_CUDA(cudaEventRecord(join_hi, hi));
     DPV_CUDA(cudaStreamWaitEvent(st, join_hi, 0));
     DPV_CUDA(cudaStreamWaitEvent(st, evR[ng - 1], 0));
+    if (!pl.dense && pl.d_rows_off) {
+        DPV_TSTART("bsub", st);
+        k_bsub_seq<<<1, 1024, 0, st>>>(A, ld, N, linv, pl.d_rows, pl.d_rows_off, T, x);
+        DPV_CHECK_LAUNCH();
+        return DPV_OK;
+    }
     const int G = std::min<int>(c.coop_blocks, 160);
     void* args[] = {&A, &ld, &N, &linv, &part, &x};
     DPV_TSTART("bsub", st);

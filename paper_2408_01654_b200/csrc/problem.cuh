@@ -15,12 +15,14 @@ struct FactorPlan {
     bool dense = true;
     int* d_rows = nullptr;            // trsm row tiles, per panel
     std::vector<int> rows_off;        // T + 1
+    int* d_rows_off = nullptr;        // device copy of rows_off
     int2* d_pairs = nullptr;          // syrk (row tile, col tile), per group: intra|next|rest
     std::vector<int> intra_off, next_off, rest_off, rest_end;
     int64_t pair_count = 0;
     double syrk_flops = 0.0;          // algorithmic flops of the planned updates
     ~FactorPlan() {
         if (d_rows) cudaFree(d_rows);
+        if (d_rows_off) cudaFree(d_rows_off);
         if (d_pairs) cudaFree(d_pairs);
     }
 };
