@@ -124,6 +124,10 @@ int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_
 int32_t dpv_problem_set_gauge(dpv_problem* prob, int32_t scale_degenerate,
                               int32_t touched_fixed0);
 int32_t dpv_problem_destroy(dpv_problem* prob);
+/* Factor plan of the reduced-system Cholesky (after the first dense solve):
+ * dense flag, 64-row tiles, planned trailing-update tiles and their flops. */
+int32_t dpv_problem_plan_info(const dpv_problem* prob, int32_t* dense, int64_t* tiles,
+                              int64_t* update_tiles, double* update_flops);
 int32_t dpv_problem_get_info(const dpv_problem* prob, dpv_problem_info* info);
 
 /* Device pointer + element count + dtype code (0=f64, 1=i32, 2=i64, 3=u8) of a

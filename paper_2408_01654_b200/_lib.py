@@ -202,3 +202,16 @@ def timing_collect() -> dict:
 SIGNATURES["dpv_problem_create_ex"] = (C.c_int32, [C.POINTER(DpvGraph), C.c_int32, C.c_int32, vp,
                                                    C.c_int64, vp, C.c_int64, vp, C.POINTER(vp)])
 SIGNATURES["dpv_problem_set_gauge"] = (C.c_int32, [vp, C.c_int32, C.c_int32])
+SIGNATURES["dpv_problem_plan_info"] = (C.c_int32, [vp, c_int32_p, c_int64_p, c_int64_p,
+                                                   C.POINTER(C.c_double)])
+
+
+def plan_info(handle) -> dict:
+    d = C.c_int32()
+    t = C.c_int64()
+    u = C.c_int64()
+    f = C.c_double()
+    check(lib().dpv_problem_plan_info(handle, C.byref(d), C.byref(t), C.byref(u), C.byref(f)),
+          "plan_info")
+    return {"dense": bool(d.value), "tiles": int(t.value), "update_tiles": int(u.value),
+            "update_flops": float(f.value)}

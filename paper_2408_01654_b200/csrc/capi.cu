@@ -368,6 +368,20 @@ int32_t dpv_problem_destroy(dpv_problem* prob) {
     return DPV_OK;
 }
 
+int32_t dpv_problem_plan_info(const dpv_problem* p, int32_t* dense, int64_t* tiles,
+                              int64_t* update_tiles, double* update_flops) {
+    DPV_ARG(p, "NULL problem");
+    if (!p->plan) {
+        set_error("no factor plan yet (built by the first dense solve)");
+        return DPV_BAD_ARGS;
+    }
+    if (dense) *dense = p->plan->dense ? 1 : 0;
+    if (tiles) *tiles = p->plan->T;
+    if (update_tiles) *update_tiles = p->plan->pair_count;
+    if (update_flops) *update_flops = p->plan->syrk_flops;
+    return DPV_OK;
+}
+
 int32_t dpv_problem_get_info(const dpv_problem* p, dpv_problem_info* info) {
     DPV_ARG(p && info, "NULL argument");
     info->n_edges = p->E;
