@@ -128,6 +128,10 @@ int32_t dpv_problem_destroy(dpv_problem* prob);
  * dense flag, 64-row tiles, planned trailing-update tiles and their flops. */
 int32_t dpv_problem_plan_info(const dpv_problem* prob, int32_t* dense, int64_t* tiles,
                               int64_t* update_tiles, double* update_flops);
+/* Sparse band+border factor plan of the reduced camera system (spd.cu):
+ * v9 = [n, chains, band tiles, tile bandwidth, border poses, border rows,
+ *       level-2 tiles, factor CTAs, modelled us]. */
+int32_t dpv_problem_spd_info(const dpv_problem* prob, int64_t* v9);
 int32_t dpv_problem_get_info(const dpv_problem* prob, dpv_problem_info* info);
 
 /* Device pointer + element count + dtype code (0=f64, 1=i32, 2=i64, 3=u8) of a
@@ -211,6 +215,14 @@ typedef struct dpv_lm_report {  /* ba.BAReport (ba.py:497-518) */
 int32_t dpv_lm_solve(dpv_problem* prob, double* q, double* t, double* d,
                      const dpv_lm_params* params, dpv_lm_report* report, void* stream);
 
+/* Block-sparse SPD solve (the block-sparse backend, block_cholesky.py:48-111
+ * + BlockCholeskyFactor.solve 31-45): keys (n_keys, 2) HOST int64 upper
+ * pattern a <= b of 6x6 blocks; blocks (n_keys, 6, 6) and rhs (6n) DEVICE
+ * f64; x (6n) DEVICE out.  Banded + border plan, one dataflow factor kernel
+ * (spd.cu).  status_dev[0] = 1 if not positive definite (SingularSystem). */
+int32_t dpv_block_sparse_solve(const int64_t* keys, int64_t n_keys, int64_t n,
+                               const double* blocks, const double* rhs, double* x,
+                               int32_t* status_dev, void* stream);
 /* ------------------------------------------------------------------------
  * Dense SPD solve (the K4c engine, usable standalone).
  * A: (N,N) row-major, lower triangle read, overwritten by L; b (N) -> x.

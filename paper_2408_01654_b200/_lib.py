@@ -85,6 +85,8 @@ SIGNATURES = {
     "dpv_lm_solve": (C.c_int32, [vp, vp, vp, vp, C.POINTER(DpvLmParams),
                                  C.POINTER(DpvLmReport), vp]),
     "dpv_cholesky_solve": (C.c_int32, [vp, vp, C.c_int64, vp, vp]),
+    "dpv_block_sparse_solve": (C.c_int32, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
+    "dpv_problem_spd_info": (C.c_int32, [vp, c_int64_p]),
     "dpv_block_fill_count": (C.c_int32, [vp, C.c_int64, C.c_int64, c_int64_p]),
     "dpv_corr": (C.c_int32, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                              C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp]),
@@ -215,3 +217,12 @@ def plan_info(handle) -> dict:
           "plan_info")
     return {"dense": bool(d.value), "tiles": int(t.value), "update_tiles": int(u.value),
             "update_flops": float(f.value)}
+
+
+def spd_info(handle) -> dict:
+    """Sparse band+border factor plan (dpv_problem_spd_info)."""
+    v = (C.c_int64 * 9)()
+    check(lib().dpv_problem_spd_info(handle, C.cast(v, c_int64_p)), "spd_info")
+    names = ("n", "chains", "band_tiles", "tile_bandwidth", "border_poses", "border_rows",
+             "level2_tiles", "factor_ctas", "model_us")
+    return {k: int(v[i]) for i, k in enumerate(names)}

@@ -371,6 +371,15 @@ int32_t dpv_problem_destroy(dpv_problem* prob) {
 int32_t dpv_problem_plan_info(const dpv_problem* p, int32_t* dense, int64_t* tiles,
                               int64_t* update_tiles, double* update_flops) {
     DPV_ARG(p, "NULL problem");
+    if (p->spd) {
+        int64_t v[9];
+        spd_plan_describe(p->spd, v);
+        if (dense) *dense = 0;
+        if (tiles) *tiles = v[2];
+        if (update_tiles) *update_tiles = v[7];
+        if (update_flops) *update_flops = spd_plan_flops(p->spd);
+        return DPV_OK;
+    }
     if (!p->plan) {
         set_error("no factor plan yet (built by the first dense solve)");
         return DPV_BAD_ARGS;
@@ -379,6 +388,16 @@ int32_t dpv_problem_plan_info(const dpv_problem* p, int32_t* dense, int64_t* til
     if (tiles) *tiles = p->plan->T;
     if (update_tiles) *update_tiles = p->plan->pair_count;
     if (update_flops) *update_flops = p->plan->syrk_flops;
+    return DPV_OK;
+}
+
+int32_t dpv_problem_spd_info(const dpv_problem* p, int64_t* v9) {
+    DPV_ARG(p && v9, "NULL argument");
+    if (!p->spd) {
+        set_error("no sparse factor plan yet (built by the first solve with n > 27)");
+        return DPV_BAD_ARGS;
+    }
+    spd_plan_describe(p->spd, v9);
     return DPV_OK;
 }
 
@@ -632,6 +651,40 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     p->lm_wd = wd;
     DPV_CUDA(cudaStreamSynchronize(st));
     return DPV_OK;
+}
+
+int32_t dpv_block_sparse_solve(const int64_t* keys, int64_t n_keys, int64_t n,
+                               const double* blocks, const double* rhs, double* x,
+                               int32_t* status_dev, void* stream) {
+    clear_error();
+    DPV_ARG(keys && blocks && rhs && x && status_dev && n >= 1 && n_keys >= 1, "NULL argument");
+    cudaStream_t st = as_stream(stream);
+    std::vector<int32_t> ka(n_keys), kb(n_keys);
+    for (int64_t w = 0; w < n_keys; ++w) {
+        const int64_t a = keys[2 * w], b = keys[2 * w + 1];
+        DPV_ARG(0 <= a && a <= b && b < n, "keys must be upper-triangle (a <= b < n)");
+        ka[w] = (int32_t)a;
+        kb[w] = (int32_t)b;
+    }
+    SpdPlan* plan = nullptr;
+    DPV_TRY(spd_plan_build(ka.data(), kb.data(), n_keys, n, &plan));
+    int32_t* dk = nullptr;
+    cudaError_t e = cudaMallocAsync(&dk, sizeof(int32_t) * 2 * n_keys, st);
+    int32_t rc = DPV_OK;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dk, ka.data(), sizeof(int32_t) * n_keys,
+                                              cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dk + n_keys, kb.data(), sizeof(int32_t) * n_keys,
+                                              cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(status_dev, 0, sizeof(int32_t) * 2, st);
+    if (e != cudaSuccess) {
+        set_error(std::string("dpv_block_sparse_solve: ") + cudaGetErrorString(e));
+        rc = DPV_CUDA_ERROR;
+    }
+    if (rc == DPV_OK) rc = spd_factor_solve(plan, dk, dk + n_keys, blocks, rhs, x, status_dev, st);
+    cudaStreamSynchronize(st);   // the plan's buffers are freed below
+    if (dk) cudaFreeAsync(dk, st);
+    spd_plan_free(plan);
+    return rc;
 }
 
 int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev, void* stream) {

@@ -27,6 +27,16 @@ struct FactorPlan {
     }
 };
 int32_t build_factor_plan(int64_t N, const std::vector<char>* tile_pattern, FactorPlan& pl);
+
+// Banded + border sparse SPD solver of the reduced camera system (spd.cu).
+struct SpdPlan;
+int32_t spd_plan_build(const int32_t* ka, const int32_t* kb, int64_t W, int64_t n, SpdPlan** out);
+void spd_plan_free(SpdPlan* p);
+int64_t spd_plan_bytes(const SpdPlan* p);
+void spd_plan_describe(const SpdPlan* p, int64_t* v);
+double spd_plan_flops(const SpdPlan* p);
+int32_t spd_factor_solve(SpdPlan* pl, const int32_t* ka, const int32_t* kb, const double* blocks,
+                         const double* rhs, double* dp, int32_t* status, cudaStream_t st);
 }  // namespace dpv
 
 struct dpv_problem {
@@ -127,6 +137,8 @@ struct dpv_problem {
     double* bsub_part = nullptr;   // back-substitution partials + diag inverses
     dpv::FactorPlan* plan = nullptr;  // tile plan of the reduced system (lazily built)
     int32_t* perm_pos = nullptr;   // (n) pose var -> permuted position in the dense solve
+    dpv::SpdPlan* spd = nullptr;   // sparse band+border solver plan (lazily built)
+    double* sblk = nullptr;        // (W, 36) S(lambda) blocks for the sparse solver
     int32_t* status = nullptr;     // (4) device flags
 
     // ---- LM scratch ------------------------------------------------------------
@@ -161,6 +173,7 @@ struct dpv_problem {
         for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
         if (lm_host) cudaFreeHost(lm_host);
         delete plan;
+        dpv::spd_plan_free(spd);
     }
 };
 

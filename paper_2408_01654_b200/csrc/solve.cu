@@ -301,6 +301,12 @@ __global__ void k_apply_step(int64_t F, int32_t first, int32_t last, int64_t P, 
 
 int64_t dense_ld(int64_t N) { return ((N + 1 + 7) / 8) * 8; }
 
+// DPV_DENSE_SOLVE=1: the dense (tile-plan) factorisation instead of spd.cu
+bool dense_solve_forced() {
+    static const bool v = getenv("DPV_DENSE_SOLVE") && atoi(getenv("DPV_DENSE_SOLVE")) != 0;
+    return v;
+}
+
 // Symmetric permutation + tile plan of the reduced camera system (host, once
 // per problem: the pattern = union_keys is state-independent).  Poses with a
 // long-range coupling (a loop-closure block farther than `band` poses from
@@ -317,7 +323,7 @@ int32_t ensure_plan(dpv_problem* p, int64_t N, cudaStream_t st) {
     std::vector<int32_t> pos(n);
     for (int64_t v = 0; v < n; ++v) pos[v] = (int32_t)v;
     const char* env = getenv("DPV_DENSE_SOLVE");
-    const bool dense = env && atoi(env) != 0;
+    const bool dense = env && atoi(env) == 1;   // 2: sparse tile plan
     auto* plan = new (std::nothrow) FactorPlan();
     DPV_ARG(plan != nullptr, "allocation failed");
     if (dense) {
@@ -417,6 +423,20 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
                                              p->schur_blocks, p->rhs_pose, p->rhs_schur, p->scal,
                                              lam, dp, status);
         DPV_CHECK_LAUNCH();
+    } else if (!dense_solve_forced()) {
+        // banded + border sparse factorisation (spd.cu)
+        if (!p->spd) {
+            std::vector<int32_t> ka(p->W), kb(p->W);
+            DPV_CUDA(cudaMemcpyAsync(ka.data(), p->key_a, sizeof(int32_t) * p->W,
+                                     cudaMemcpyDeviceToHost, st));
+            DPV_CUDA(cudaMemcpyAsync(kb.data(), p->key_b, sizeof(int32_t) * p->W,
+                                     cudaMemcpyDeviceToHost, st));
+            DPV_CUDA(cudaStreamSynchronize(st));
+            DPV_TRY(spd_plan_build(ka.data(), kb.data(), p->W, p->n, &p->spd));
+            DPV_TRY(p->alloc(&p->sblk, p->W * 36));
+        }
+        DPV_TRY(reduced_system(p, lam, p->sblk, p->red_rhs, nullptr, st));
+        DPV_TRY(spd_factor_solve(p->spd, p->key_a, p->key_b, p->sblk, p->red_rhs, dp, status, st));
     } else {
         DPV_TRY(ensure_dense(p, N, st));
         const int64_t ld = p->dense_ld;
