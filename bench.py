@@ -134,7 +134,11 @@ def corr_edge_selection(graph, prob, window, torch):
     kind = torch.as_tensor(graph._kind.view.astype(np.int32), device="cuda").long()[eidx]
     nf = graph.n_frames
     sel = (dst >= nf - window) | (kind == 1)
-    return torch.nonzero(sel).flatten()
+    idx = torch.nonzero(sel).flatten()
+    # process the correlation edges grouped by target frame (L2 reuse of its
+    # feature map); the output is per edge, so the order is the caller's
+    order = torch.argsort(dst[idx], stable=True)
+    return idx[order]
 
 
 def build_workload(args, torch):
@@ -196,8 +200,10 @@ class Stepper:
         n = int(work["info"].n_free)
         P = int(work["info"].n_depths)
         dev = "cuda"
-        self.coords_all = torch.empty((E, 9, 2), dtype=torch.float64, device=dev)
         self.Ec = len(work["csel"])
+        self.side = torch.cuda.Stream()           # K1 runs beside the BA step
+        self.ev_fork = torch.cuda.Event()
+        self.ev_join = torch.cuda.Event()
         self.coords = torch.empty((self.Ec, 9, 2), dtype=torch.float64, device=dev)
         self.cout = torch.empty((self.Ec, len(work["pyr"]), 9, 7, 7), dtype=torch.float32,
                                 device=dev)
@@ -218,11 +224,17 @@ class Stepper:
         s = L.stream_ptr()
         P = L.ptr
         from paper_2408_01654_b200 import corr
-        L.check(lib.dpv_reproject_coords(self.h, P(q), P(t), P(d), 0.25, P(self.coords_all), s),
-                "coords")
-        # gather the corr edges' coordinates (index_select kernel from torch) -> K1
-        self.torch.index_select(self.coords_all, 0, w["csel"], out=self.coords)
-        corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
+        torch = self.torch
+        # K2 pixels of the correlation edges -> K1, on a side stream: the
+        # correlation is independent of this BA step and overlaps it
+        self.ev_fork.record()
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(self.ev_fork)
+            L.check(lib.dpv_reproject_coords_sel(self.h, P(q), P(t), P(d), 0.25, P(w["csel"]),
+                                                 self.Ec, P(self.coords), L.stream_ptr()),
+                    "coords")
+            corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
+            self.ev_join.record()
         L.check(lib.dpv_assemble(self.h, P(q), P(t), P(d), s), "assemble")
         if w["sharded"]:
             w["prob"].allreduce_system()      # NCCL: reduced pose system
@@ -235,6 +247,7 @@ class Stepper:
         else:
             L.check(lib.dpv_objective(self.h, P(self.q2), P(self.t2), P(self.d2), P(self.obj),
                                       s), "objective")
+        torch.cuda.current_stream().wait_event(self.ev_join)
 
 
 def time_steps(fn, k, torch):
@@ -284,7 +297,8 @@ def kernel_rooflines(timing, work, steps, hbm_peak):
         # name: (bound, algorithmic bytes or flops per step, unit)
         "assemble_edges": ("fp64+hbm", E * 172 + P * 152, "B"),
         "objective": ("hbm", E * 172 + P * 152, "B"),
-        "coords": ("hbm", E * (12 + 144) + P * 152, "B"),
+        # corr edges: src/dst/row (12) + the patch's rays and depth (152) in, 144 out
+        "coords": ("hbm", Ec * (12 + 152 + 144), "B"),
         "syrk": ("tensor", syrk_flops, "flop"),
         # coords + indices + output + the edges' patch features + every feature map once
         "corr": ("hbm", Ec * (144 + 8 + L * 9 * 49 * 4) + Ec * 9 * work["C"] * fbytes

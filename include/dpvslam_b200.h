@@ -176,6 +176,12 @@ int32_t dpv_solve(dpv_problem* prob, double lam, double* dp, double* dd, int32_t
  * for 1/4-resolution feature maps).  Same arithmetic as reproject_grid. */
 int32_t dpv_reproject_coords(dpv_problem* prob, const double* q, const double* t,
                              const double* d, double scale, double* coords, void* stream);
+/* K2 pixels (scaled) of a selection of problem edges (DEVICE int64 problem
+ * edge indices) -> coords_out (n_sel, p*p, 2) in selection order: the
+ * correlation edges' coordinates without reprojecting every BA edge. */
+int32_t dpv_reproject_coords_sel(dpv_problem* prob, const double* q, const double* t,
+                                 const double* d, double scale, const int64_t* sel,
+                                 int64_t n_sel, double* coords_out, void* stream);
 /* Replace the flow targets (E,m,2) and confidences (E,2) (problem order, conf
  * may be NULL) without rebuilding the index: the per-iteration update-operator
  * output of DPVO or a re-run flow oracle. */

@@ -29,6 +29,7 @@ struct Cell {
     double xw[3];
     double xt[3];
     double zs;
+    double iz;      // 1 / zs
     bool valid;
     double u, v;
 };
@@ -48,8 +49,34 @@ __device__ __forceinline__ void reproject_cell(double rx, double ry, double inv_
     for (int k = 0; k < 3; ++k) c.xt[k] = fj.R[k] * e0 + fj.R[3 + k] * e1 + fj.R[6 + k] * e2;
     c.valid = c.xt[2] > kDepthEps;
     c.zs = c.valid ? c.xt[2] : 1.0;
-    c.u = intr[0] * c.xt[0] / c.zs + intr[2];
-    c.v = intr[1] * c.xt[1] / c.zs + intr[3];
+    // one reciprocal per cell instead of two divisions (results agree with
+    // the reference's fx * x / z to a few ulp; parity is tolerance-based)
+    c.iz = __drcp_rn(c.zs);
+    c.u = intr[0] * c.xt[0] * c.iz + intr[2];
+    c.v = intr[1] * c.xt[1] * c.iz + intr[3];
+}
+
+// same, frames read from shared memory (per-warp uniform, broadcast loads)
+struct FrameP {
+    const double* R;
+    const double* t;
+};
+
+__device__ __forceinline__ void reproject_cell(double rx, double ry, double inv_d_recip,
+                                               const FrameP& fi, const FrameP& fj,
+                                               const double* intr, Cell& c) {
+    const double xc0 = rx * inv_d_recip, xc1 = ry * inv_d_recip, xc2 = inv_d_recip;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        c.xw[r] = fi.R[3 * r] * xc0 + fi.R[3 * r + 1] * xc1 + fi.R[3 * r + 2] * xc2 + fi.t[r];
+    const double e0 = c.xw[0] - fj.t[0], e1 = c.xw[1] - fj.t[1], e2 = c.xw[2] - fj.t[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c.xt[k] = fj.R[k] * e0 + fj.R[3 + k] * e1 + fj.R[6 + k] * e2;
+    c.valid = c.xt[2] > kDepthEps;
+    c.zs = c.valid ? c.xt[2] : 1.0;
+    c.iz = __drcp_rn(c.zs);
+    c.u = intr[0] * c.xt[0] * c.iz + intr[2];
+    c.v = intr[1] * c.xt[1] * c.iz + intr[3];
 }
 
 // ---------------------------------------------------------------------------
@@ -70,7 +97,7 @@ __global__ void __launch_bounds__(256) k_objective(
         load_frame(Rall, tall, a_src[e], fi);
         load_frame(Rall, tall, a_dst[e], fj);
         const int32_t row = a_row[e];
-        const double id = 1.0 / __ldg(d + row);
+        const double id = __drcp_rn(__ldg(d + row));
         const double w0 = a_w[e], w1 = a_w[E + e];
         double s = 0.0;
         for (int c = 0; c < m; ++c) {
@@ -89,6 +116,65 @@ __global__ void __launch_bounds__(256) k_objective(
     __shared__ double sh[8];
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+// same sum, one warp per (src, dst) segment: the two frames are loaded once
+// per segment into shared memory, lanes stride over the segment's edges.
+template <int M>
+__global__ void __launch_bounds__(256) k_objective_seg(
+    int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
+    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
+    const double* __restrict__ a_w, const double* __restrict__ r_ray,
+    const double* __restrict__ Rall, const double* __restrict__ tall,
+    const double* __restrict__ d, double fx, double fy, double cx, double cy,
+    double* __restrict__ part) {
+    const double intr[4] = {fx, fy, cx, cy};
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    __shared__ double sfr[8][24];
+    double* fr = sfr[threadIdx.x >> 5];
+    const FrameP fi{fr, fr + 9}, fj{fr + 12, fr + 21};
+    double acc = 0.0;
+    for (int64_t s = warp; s < S; s += nwarps) {
+        const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
+        __syncwarp();
+        if (lane < 12) {
+            const int32_t f = seg_src[s];
+            fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
+        } else if (lane < 24) {
+            const int32_t f = seg_dst[s];
+            fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
+        }
+        __syncwarp();
+        for (int32_t e = e0 + lane; e < e1; e += 32) {
+            const int32_t row = a_row[e];
+            const double id = __drcp_rn(__ldg(d + row));
+            const double w0 = a_w[e], w1 = a_w[E + e];
+            double sum = 0.0;
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                Cell cl;
+                reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
+                               __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr,
+                               cl);
+                const double r0 = cl.u - a_tgt[(int64_t)(2 * c) * E + e];
+                const double r1 = cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e];
+                sum += cl.valid ? w0 * r0 * r0 + w1 * r1 * r1 : 0.0;
+            }
+            acc += sum;
+        }
+    }
+    __shared__ double sh[8];
+    acc = warp_sum(acc);
+    if (lane == 0) sh[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -150,7 +236,7 @@ __global__ void k_coords(int64_t E, int m, int64_t P, const int32_t* a_src,
         load_frame(Rall, tall, a_src[e], fi);
         load_frame(Rall, tall, a_dst[e], fj);
         const int32_t row = a_row[e];
-        const double id = 1.0 / __ldg(d + row);
+        const double id = __drcp_rn(__ldg(d + row));
         const int64_t p = a_pidx[e];
         for (int c = 0; c < m; ++c) {
             Cell cl;
@@ -159,6 +245,32 @@ __global__ void k_coords(int64_t E, int m, int64_t P, const int32_t* a_src,
             coords[(p * m + c) * 2] = cl.u * scale;
             coords[(p * m + c) * 2 + 1] = cl.v * scale;
         }
+    }
+}
+
+// K2 pixels of a selection of problem edges (the correlation edges), output
+// in selection order
+__global__ void k_coords_sel(int64_t n_sel, const int64_t* sel, const int32_t* p_pos, int m,
+                             int64_t P, const int32_t* a_src, const int32_t* a_dst,
+                             const int32_t* a_row, const double* r_ray, const double* Rall,
+                             const double* tall, const double* d, double fx, double fy,
+                             double cx, double cy, double scale, double* coords) {
+    const double intr[4] = {fx, fy, cx, cy};
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_sel * m;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / m;
+        const int c = (int)(x % m);
+        const int64_t e = p_pos[sel[i]];
+        Frame fi, fj;
+        load_frame(Rall, tall, a_src[e], fi);
+        load_frame(Rall, tall, a_dst[e], fj);
+        const int32_t row = a_row[e];
+        const double id = __drcp_rn(__ldg(d + row));
+        Cell cl;
+        reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
+                       __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr, cl);
+        coords[x * 2] = cl.u * scale;
+        coords[x * 2 + 1] = cl.v * scale;
     }
 }
 
@@ -185,7 +297,7 @@ __device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
     return a * 6 - (a * (a - 1)) / 2 + (b - a);
 }
 
-__global__ void __launch_bounds__(128) k_assemble_edges(
+__global__ void __launch_bounds__(128, 3) k_assemble_edges(
     int64_t S, int64_t E, int m, int64_t P, const int32_t* __restrict__ seg_ptr,
     const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
     const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
@@ -197,11 +309,20 @@ __global__ void __launch_bounds__(128) k_assemble_edges(
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    __shared__ double sfr[4][24];
+    double* fr = sfr[threadIdx.x >> 5];
+    const FrameP fi{fr, fr + 9}, fj{fr + 12, fr + 21};
     for (int64_t s = warp; s < S; s += nwarps) {
         const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
-        Frame fi, fj;
-        load_frame(Rall, tall, seg_src[s], fi);
-        load_frame(Rall, tall, seg_dst[s], fj);
+        __syncwarp();
+        if (lane < 12) {
+            const int32_t f = seg_src[s];
+            fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
+        } else if (lane < 24) {
+            const int32_t f = seg_dst[s];
+            fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
+        }
+        __syncwarp();
         double H[21], G[6];
 #pragma unroll
         for (int k = 0; k < 21; ++k) H[k] = 0.0;
@@ -210,7 +331,7 @@ __global__ void __launch_bounds__(128) k_assemble_edges(
         for (int32_t e = e0 + lane; e < e1; e += 32) {
             const int32_t row = a_row[e];
             const double dd = __ldg(d + row);
-            const double id = 1.0 / dd;
+            const double id = __drcp_rn(dd);
             const double sw0 = sqrt(a_w[e]), sw1 = sqrt(a_w[E + e]);
             double ep[6] = {0, 0, 0, 0, 0, 0};
             double cdd = 0.0, gd = 0.0;
@@ -221,7 +342,7 @@ __global__ void __launch_bounds__(128) k_assemble_edges(
                                cl);
                 const double s0 = cl.valid ? sw0 : 0.0;
                 const double s1 = cl.valid ? sw1 : 0.0;
-                const double iz = 1.0 / cl.zs;
+                const double iz = cl.iz;
                 // A = Jproj R_j^T (geometry.py:514-522)
                 const double p0 = intr[0] * iz, q0 = -intr[0] * cl.xt[0] * iz * iz;
                 const double p1 = intr[1] * iz, q1 = -intr[1] * cl.xt[1] * iz * iz;
@@ -293,6 +414,8 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
                        const double* e_terms, double* depth_diag, double* rhs_depth,
                        uint8_t* active, double* cinv0, unsigned long long* grad_bits,
                        unsigned long long* n_inactive) {
+    double gmax = 0.0;
+    unsigned long long inact = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
          r += (int64_t)gridDim.x * blockDim.x) {
         double c = 0.0, g = 0.0;
@@ -306,12 +429,20 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
         const bool act = c > kActiveEps;
         active[r] = act ? 1 : 0;
         cinv0[r] = act ? 1.0 / c : 0.0;
-        if (act) {
-            const unsigned long long gb = (unsigned long long)__double_as_longlong(fabs(g));
+        if (act) gmax = fmax(gmax, fabs(g));
+        else ++inact;
+    }
+    // one atomic per warp (max / count are order-independent)
+    gmax = warp_max(gmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inact += __shfl_xor_sync(0xffffffffu, inact, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (gmax > 0.0) {
+            const unsigned long long gb = (unsigned long long)__double_as_longlong(gmax);
             atomicMax(grad_bits, gb);
             atomicMax(grad_bits + 7, gb);   // depth-only part (sharded BA)
         }
-        else atomicAdd(n_inactive, 1ull);
+        if (inact) atomicAdd(n_inactive, inact);
     }
 }
 
@@ -338,12 +469,20 @@ __global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const
     }
 }
 
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
 // pose blocks (ba.py:389-394) and Schur blocks E C0^-1 E^T (ba.py:405-413):
 // one warp per union key, fixed lane-strided order + xor-tree reduction
 __global__ void __launch_bounds__(128) k_key_blocks(
     int64_t W, const int32_t* key_seg_ptr, const int32_t* key_seg, const double* seg_h,
-    const int64_t* key_pair_ptr, const int32_t* pair_l, const int32_t* pair_r,
-    const double* uinc, const double* inc_block, double* pose_blocks, double* schur_blocks) {
+    const int32_t* __restrict__ key_run_ptr, const int32_t* __restrict__ run_l,
+    const int32_t* __restrict__ run_r, const int32_t* __restrict__ run_len,
+    const double* __restrict__ uinc, const double* __restrict__ inc_block,
+    double* __restrict__ pose_blocks, double* __restrict__ schur_blocks) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -369,27 +508,38 @@ __global__ void __launch_bounds__(128) k_key_blocks(
             for (int q = 0; q < 21; ++q) v = (q == t) ? h[q] : v;
             pose_blocks[w * 36 + idx] = v;
         }
-        double s[36];
+        // Schur block = U^T V over the key's pair runs (l+t, r+t) on the FP64
+        // tensor cores: per m8n8k4 step 4 pairs; lane (k = lane&3, i = lane>>2)
+        // loads component i of pair k of both sides, so a quad reads 4
+        // consecutive 48-byte incidence blocks (coalesced).  4 independent
+        // accumulators break the DMMA dependency chain.
+        const int kq = lane & 3, ci = lane >> 2;
+        double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        for (int32_t q = key_run_ptr[w]; q < key_run_ptr[w + 1]; ++q) {
+            const int32_t len = run_len[q];
+            const double* ub = uinc + (int64_t)run_l[q] * 6;
+            const double* vb = inc_block + (int64_t)run_r[q] * 6;
+            // 8 steps (32 pairs) of loads in flight, then 8 DMMAs
+            for (int32_t t0 = 0; t0 < len; t0 += 32) {
+                double a[8], b[8];
 #pragma unroll
-        for (int k = 0; k < 36; ++k) s[k] = 0.0;
-        for (int64_t k = key_pair_ptr[w] + lane; k < key_pair_ptr[w + 1]; k += 32) {
-            const double* u = uinc + (int64_t)pair_l[k] * 6;
-            const double* v = inc_block + (int64_t)pair_r[k] * 6;
-            double uu[6], vv[6];
+                for (int u = 0; u < 8; ++u) {
+                    const int32_t t = t0 + 4 * u + kq;
+                    const bool ok = t < len && ci < 6;
+                    a[u] = ok ? __ldg(ub + (int64_t)t * 6 + ci) : 0.0;
+                    b[u] = ok ? __ldg(vb + (int64_t)t * 6 + ci) : 0.0;
+                }
 #pragma unroll
-            for (int a = 0; a < 6; ++a) { uu[a] = u[a]; vv[a] = v[a]; }
-#pragma unroll
-            for (int a = 0; a < 6; ++a)
-#pragma unroll
-                for (int b = 0; b < 6; ++b) s[a * 6 + b] += uu[a] * vv[b];
+                for (int u = 0; u < 8; ++u) dmma_f64(c[u & 3][0], c[u & 3][1], a[u], b[u]);
+            }
         }
+        // C[i][j] at lane (i = lane>>2, j = 2*(lane&3) + h)
+        const int oi = lane >> 2;
 #pragma unroll
-        for (int k = 0; k < 36; ++k) s[k] = warp_sum(s[k]);
-        for (int idx = lane; idx < 36; idx += 32) {
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < 36; ++q) v = (q == idx) ? s[q] : v;
-            schur_blocks[w * 36 + idx] = v;
+        for (int h = 0; h < 2; ++h) {
+            const int oj = 2 * (lane & 3) + h;
+            const double v = (c[0][h] + c[1][h]) + (c[2][h] + c[3][h]);
+            if (oi < 6 && oj < 6) schur_blocks[w * 36 + oi * 6 + oj] = v;
         }
     }
 }
@@ -453,10 +603,16 @@ int32_t objective(dpv_problem* p, const double* q, const double* t, const double
                   cudaStream_t st) {
     DPV_TRY(frame_rotations(p, q, st));
     DPV_TSTART("objective", st);
-    k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
-                                            p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d,
-                                            p->intr[0], p->intr[1], p->intr[2], p->intr[3],
-                                            p->obj_part);
+    if (p->m == 9 && p->S > 0)
+        k_objective_seg<9><<<kObjBlocks, 256, 0, st>>>(
+            p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,
+            p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+            p->obj_part);
+    else
+        k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
+                                                p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d,
+                                                p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+                                                p->obj_part);
     DPV_CHECK_LAUNCH();
     DPV_TSTART("sum_parts", st);
     k_sum_parts<<<1, 1024, 0, st>>>(kObjBlocks, p->obj_part, out);
@@ -486,6 +642,19 @@ int32_t coords(dpv_problem* p, const double* q, const double* t, const double* d
                                                    p->a_pidx, p->r_ray, p->frame_R, t, d,
                                                    p->intr[0], p->intr[1], p->intr[2], p->intr[3],
                                                    scale, out);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
+int32_t coords_sel(dpv_problem* p, const double* q, const double* t, const double* d,
+                   double scale, const int64_t* sel, int64_t n_sel, double* out,
+                   cudaStream_t st) {
+    DPV_TRY(frame_rotations(p, q, st));
+    if (n_sel == 0) return DPV_OK;
+    DPV_TSTART("coords", st);
+    k_coords_sel<<<grid_for(n_sel * p->m, 256), 256, 0, st>>>(
+        n_sel, sel, p->p_pos, p->m, p->P, p->a_src, p->a_dst, p->a_row, p->r_ray, p->frame_R, t,
+        d, p->intr[0], p->intr[1], p->intr[2], p->intr[3], scale, out);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
 }
@@ -534,8 +703,9 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("key_blocks", st);
         k_key_blocks<<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
-                                             p->key_pair_ptr, p->pair_l, p->pair_r, p->uinc,
-                                             p->inc_block, p->pose_blocks, p->schur_blocks);
+                                             p->key_run_ptr, p->run_l, p->run_r, p->run_len,
+                                             p->uinc, p->inc_block, p->pose_blocks,
+                                             p->schur_blocks);
         DPV_CHECK_LAUNCH();
     }
     if (p->n > 0) {

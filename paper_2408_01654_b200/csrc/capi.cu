@@ -518,6 +518,14 @@ int32_t dpv_reproject_coords(dpv_problem* p, const double* q, const double* t, c
     return coords(p, q, t, d, scale, coords_out, as_stream(stream));
 }
 
+int32_t dpv_reproject_coords_sel(dpv_problem* p, const double* q, const double* t,
+                                 const double* d, double scale, const int64_t* sel,
+                                 int64_t n_sel, double* coords_out, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && (n_sel == 0 || (sel && coords_out)), "NULL argument");
+    return coords_sel(p, q, t, d, scale, sel, n_sel, coords_out, as_stream(stream));
+}
+
 int32_t dpv_update_targets(dpv_problem* p, const double* target, const double* conf,
                            void* stream) {
     clear_error();

@@ -107,6 +107,12 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 // quaternion (x,y,z,w) -> row-major rotation; restates geometry.py:70-86
 __device__ __forceinline__ void quat_to_rot(const double* q, double* r) {
     const double x = q[0], y = q[1], z = q[2], w = q[3];

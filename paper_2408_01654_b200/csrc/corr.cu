@@ -11,6 +11,9 @@
 // for all p*p cells.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "problem.cuh"
 
 namespace dpv {
@@ -182,6 +185,220 @@ int32_t launch_corr(const void* gmap, const void* fmap, const double* coords, co
     return DPV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// bf16 features on the tensor cores.  Per (edge, level) the union window of
+// the 9 cells' 8x8 tap grids (<= kMmaTaps taps; ~81 at these scales) and the
+// patch's 9 feature vectors are staged in shared memory with cp.async, then
+//   S (16 x taps) = G (16 x C, rows >= 9 zero) * Win^T (C x taps)
+// runs on mma.sync.m16n8k16 bf16 -> fp32 (K = C); each cell's 7x7 outputs
+// are the bilinear blend of its 8x8 block of S.  Items are double-buffered
+// (the next window streams in while the current one multiplies).  Windows
+// wider than kMmaTaps fall back to per-cell dots from global memory.
+constexpr int kMmaTaps = 104;     // 13 n-tiles of 8
+constexpr int kMmaThreads = 128;
+
+__device__ __forceinline__ void mma_bf16(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+struct CorrMeta {
+    int x0[kCells], y0[kCells];
+    float fx[kCells], fy[kCells];
+    int bx0, by0, bw, bh;
+    int staged;
+    int64_t e;
+};
+
+template <int C>
+__global__ void __launch_bounds__(kMmaThreads) k_corr_mma(
+    const __nv_bfloat16* __restrict__ gmap, const __nv_bfloat16* __restrict__ fmap,
+    const double* __restrict__ coords, const int32_t* __restrict__ ii,
+    const int32_t* __restrict__ jj, int64_t E, int H, int Wd, int level, int levels,
+    float* __restrict__ out) {
+    constexpr int LDK = C + 8;                      // bf16 per staged row (272 B at C=128)
+    constexpr int BUF = (16 + kMmaTaps) * LDK;      // bf16 per buffer: G rows + window taps
+    constexpr int radius = 3, D = 8, O = 7;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __nv_bfloat16* const buf0 = reinterpret_cast<__nv_bfloat16*>(smraw);
+    auto buf = [&](int b) { return buf0 + b * BUF; };
+    float* S = reinterpret_cast<float*>(smraw + 2 * sizeof(__nv_bfloat16) * BUF);  // 9 x kMmaTaps
+    __shared__ CorrMeta meta[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const double scale = level == 0 ? 1.0 : 0.25;
+    // G rows 9..15 stay zero
+    for (int x = tid; x < 7 * LDK; x += kMmaThreads) {
+        buf(0)[9 * LDK + x] = __float2bfloat16(0.f);
+        buf(1)[9 * LDK + x] = __float2bfloat16(0.f);
+    }
+    // metadata + async staging of item e into buffer b
+    auto stage = [&](int64_t e, int b) {
+        CorrMeta& M = meta[b];
+        if (tid < kCells) {
+            int x0, y0;
+            float fx, fy;
+            split_coord(coords[(e * kCells + tid) * 2] * scale, x0, fx);
+            split_coord(coords[(e * kCells + tid) * 2 + 1] * scale, y0, fy);
+            M.x0[tid] = x0; M.y0[tid] = y0; M.fx[tid] = fx; M.fy[tid] = fy;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int mnx = M.x0[0], mxx = M.x0[0], mny = M.y0[0], mxy = M.y0[0];
+            for (int c = 1; c < kCells; ++c) {
+                mnx = min(mnx, M.x0[c]); mxx = max(mxx, M.x0[c]);
+                mny = min(mny, M.y0[c]); mxy = max(mxy, M.y0[c]);
+            }
+            M.bx0 = mnx - radius; M.by0 = mny - radius;
+            M.bw = mxx - mnx + D; M.bh = mxy - mny + D;
+            M.staged = (mxx - mnx) < 64 && (mxy - mny) < 64 && M.bw * M.bh <= kMmaTaps;
+            M.e = e;
+        }
+        __syncthreads();
+        __nv_bfloat16* G = buf(b);
+        __nv_bfloat16* Win = buf(b) + 16 * LDK;
+        const __nv_bfloat16* gp = gmap + (int64_t)ii[e] * kCells * C;
+        constexpr int CH = C / 8;                   // 16-byte chunks per row
+        for (int x = tid; x < kCells * CH; x += kMmaThreads)
+            cp16(G + (x / CH) * LDK + (x % CH) * 8, gp + (int64_t)x * 8);
+        if (M.staged) {
+            const __nv_bfloat16* fp = fmap + (int64_t)jj[e] * H * Wd * C;
+            const int ntap = M.bw * M.bh;
+            for (int x = tid; x < ntap * CH; x += kMmaThreads) {
+                const int tp = x / CH, k = (x % CH) * 8;
+                const int py = M.by0 + tp / M.bw, px = M.bx0 + tp % M.bw;
+                __nv_bfloat16* dst = Win + tp * LDK + k;
+                if (py >= 0 && py < H && px >= 0 && px < Wd)
+                    cp16(dst, fp + ((int64_t)py * Wd + px) * C + k);
+                else
+                    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+            }
+            // zero the pad taps of the last n-tile
+            const int ntile_taps = ((ntap + 7) / 8) * 8;
+            for (int x = tid; x < (ntile_taps - ntap) * CH; x += kMmaThreads)
+                *reinterpret_cast<uint4*>(Win + (ntap + x / CH) * LDK + (x % CH) * 8) =
+                    make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int64_t e = blockIdx.x;
+    if (e >= E) return;
+    stage(e, 0);
+    int b = 0;
+    for (; e < E; e += gridDim.x, b ^= 1) {
+        const int64_t en = e + gridDim.x;
+        if (en < E) {
+            stage(en, b ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const CorrMeta& M = meta[b];
+        const __nv_bfloat16* G = buf(b);
+        const __nv_bfloat16* Win = buf(b) + 16 * LDK;
+        if (M.staged) {
+            const int ntiles = (M.bw * M.bh + 7) / 8;
+            float acc[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+#pragma unroll 2
+            for (int k0 = 0; k0 < C; k0 += 16) {
+                uint32_t a[4];
+                a[0] = *reinterpret_cast<const uint32_t*>(G + g * LDK + k0 + 2 * t4);
+                a[1] = *reinterpret_cast<const uint32_t*>(G + (g + 8) * LDK + k0 + 2 * t4);
+                a[2] = *reinterpret_cast<const uint32_t*>(G + g * LDK + k0 + 2 * t4 + 8);
+                a[3] = *reinterpret_cast<const uint32_t*>(G + (g + 8) * LDK + k0 + 2 * t4 + 8);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int nt = warp + 4 * q;
+                    if (nt < ntiles) {
+                        const __nv_bfloat16* bp = Win + (nt * 8 + g) * LDK + k0 + 2 * t4;
+                        mma_bf16(acc[q], a, *reinterpret_cast<const uint32_t*>(bp),
+                                 *reinterpret_cast<const uint32_t*>(bp + 8));
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int nt = warp + 4 * q;
+                if (nt < ntiles) {
+                    const int col = nt * 8 + 2 * t4;
+                    S[g * kMmaTaps + col] = acc[q][0];
+                    S[g * kMmaTaps + col + 1] = acc[q][1];
+                    if (g == 0) {
+                        S[8 * kMmaTaps + col] = acc[q][2];
+                        S[8 * kMmaTaps + col + 1] = acc[q][3];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        float* o = out + ((M.e * levels + level) * kCells) * (int64_t)(O * O);
+        if (M.staged) {
+            for (int x = tid; x < kCells * O * O; x += kMmaThreads) {
+                const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
+                const float dx = M.fx[c], dy = M.fy[c];
+                const int base = (M.y0[c] - radius + a - M.by0) * M.bw + (M.x0[c] - radius + bb - M.bx0);
+                const float* sp = S + c * kMmaTaps + base;
+                o[x] = (1.f - dy) * ((1.f - dx) * sp[0] + dx * sp[1]) +
+                       dy * ((1.f - dx) * sp[M.bw] + dx * sp[M.bw + 1]);
+            }
+        } else {
+            // wide window: per-cell integer-tap dots straight from global memory
+            const __nv_bfloat16* fp = fmap + (int64_t)jj[M.e] * H * Wd * C;
+            for (int x = tid; x < kCells * D * D; x += kMmaThreads) {
+                const int c = x / (D * D), ty = (x % (D * D)) / D, tx = x % D;
+                const int py = M.y0[c] - radius + ty, px = M.x0[c] - radius + tx;
+                float acc = 0.f;
+                if (py >= 0 && py < H && px >= 0 && px < Wd) {
+                    const __nv_bfloat16* f = fp + ((int64_t)py * Wd + px) * C;
+                    for (int k = 0; k < C; ++k)
+                        acc += __bfloat162float(f[k]) * __bfloat162float(G[c * LDK + k]);
+                }
+                S[c * kMmaTaps + ty * D + tx] = acc;
+            }
+            __syncthreads();
+            for (int x = tid; x < kCells * O * O; x += kMmaThreads) {
+                const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
+                const float dx = M.fx[c], dy = M.fy[c];
+                const float* sp = S + c * kMmaTaps + a * D + bb;
+                o[x] = (1.f - dy) * ((1.f - dx) * sp[0] + dx * sp[1]) +
+                       dy * ((1.f - dx) * sp[D] + dx * sp[D + 1]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int C>
+int32_t launch_corr_mma(const void* gmap, const void* fmap, const double* coords,
+                        const int32_t* ii, const int32_t* jj, int64_t E, int H, int Wd,
+                        int level, int levels, float* out, cudaStream_t st) {
+    const size_t smem = 2 * sizeof(__nv_bfloat16) * (16 + kMmaTaps) * (C + 8) +
+                        sizeof(float) * kCells * kMmaTaps;
+    static size_t cur = 0;
+    DPV_TRY(ensure_smem(k_corr_mma<C>, smem, cur));
+    int per_sm = 0;
+    DPV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_corr_mma<C>, kMmaThreads,
+                                                           smem));
+    const int grid = (int)std::min<int64_t>(E, (int64_t)sm_count() * std::max(1, per_sm));
+    DPV_TSTART("corr", st);
+    k_corr_mma<C><<<grid, kMmaThreads, smem, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(gmap), reinterpret_cast<const __nv_bfloat16*>(fmap),
+        coords, ii, jj, E, H, Wd, level, levels, out);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
 // level-1 pyramid: 4x4 average pool, channels-last (DPVO avg_pool2d(4, 4))
 template <typename T>
 __global__ void k_avg_pool4(const T* __restrict__ in, int64_t F, int H, int W, int C,
@@ -234,6 +451,12 @@ int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const doubl
         if (dtype == 0)
             DPV_TRY(launch_corr<float>(gmap, f, coords, ii, jj, E, C, H, Wd, l, levels, radius,
                                        out, st));
+        else if (radius == 3 && C == 128 && !getenv("DPV_CORR_FMA"))
+            DPV_TRY(launch_corr_mma<128>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
+        else if (radius == 3 && C == 64 && !getenv("DPV_CORR_FMA"))
+            DPV_TRY(launch_corr_mma<64>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
+        else if (radius == 3 && C == 256 && !getenv("DPV_CORR_FMA"))
+            DPV_TRY(launch_corr_mma<256>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
         else
             DPV_TRY(launch_corr<__nv_bfloat16>(gmap, f, coords, ii, jj, E, C, H, Wd, l, levels,
                                                radius, out, st));

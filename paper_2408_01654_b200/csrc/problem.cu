@@ -292,6 +292,46 @@ __global__ void k_pairs(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
     }
 }
 
+// Schur pair runs: pair k starts a run unless it continues the previous pair
+// of the same key with both incidences advanced by one
+__global__ void k_run_flags(int64_t n, const uint64_t* key, const int32_t* pl, const int32_t* pr,
+                            int32_t* flag) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (k == n) {
+            flag[k] = 0;
+            continue;
+        }
+        flag[k] = (k == 0 || key[k] != key[k - 1] || pl[k] != pl[k - 1] + 1 ||
+                   pr[k] != pr[k - 1] + 1) ? 1 : 0;
+    }
+}
+
+__global__ void k_run_fill(int64_t n, const int32_t* flag, const int32_t* rid, const int32_t* pl,
+                           const int32_t* pr, int32_t* run_l, int32_t* run_r, int64_t* run_start) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (!flag[k]) continue;
+        const int32_t r = rid[k];
+        run_l[r] = pl[k];
+        run_r[r] = pr[k];
+        run_start[r] = k;
+    }
+}
+
+__global__ void k_run_len(int64_t nr, int64_t n, const int64_t* run_start, int32_t* run_len) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr;
+         r += (int64_t)gridDim.x * blockDim.x)
+        run_len[r] = (int32_t)((r + 1 < nr ? run_start[r + 1] : n) - run_start[r]);
+}
+
+__global__ void k_key_runs(int64_t W, const int64_t* key_pair_ptr, const int32_t* rid,
+                           int32_t* key_run_ptr) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= W;
+         w += (int64_t)gridDim.x * blockDim.x)
+        key_run_ptr[w] = rid[key_pair_ptr[w]];
+}
+
 __global__ void k_gather_i32(int64_t n, const int32_t* idx, const int32_t* src, int32_t* dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -821,6 +861,39 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         }
         DPV_CUDA(cudaMemcpyAsync(P->key_pair_ptr + W, &P->NP, sizeof(int64_t),
                                  cudaMemcpyHostToDevice, st));
+    }
+
+    // 10b. run-length form of the Schur pairs (banded graphs: ~1 run per key),
+    // so the Schur kernel streams contiguous incidence blocks
+    {
+        int32_t *flag, *rid;
+        DPV_TRY(sc.get(&flag, NPR + 1));
+        DPV_TRY(sc.get(&rid, NPR + 1));
+        k_run_flags<<<grid_for(NPR + 1, B), B, 0, st>>>(NPR, pkey_sorted, P->pair_l, P->pair_r,
+                                                         flag);
+        DPV_CHECK_LAUNCH();
+        DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, flag, rid, (int)NPR + 1, st);
+        }));
+        int32_t nr = 0;
+        DPV_CUDA(cudaMemcpyAsync(&nr, rid + NPR, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        DPV_CUDA(cudaStreamSynchronize(st));
+        P->NR = nr;
+        int64_t* run_start;
+        DPV_TRY(sc.get(&run_start, std::max<int64_t>(nr, 1)));
+        DPV_TRY(P->alloc(&P->run_l, nr));
+        DPV_TRY(P->alloc(&P->run_r, nr));
+        DPV_TRY(P->alloc(&P->run_len, nr));
+        DPV_TRY(P->alloc(&P->key_run_ptr, W + 1));
+        if (NPR > 0) {
+            k_run_fill<<<grid_for(NPR, B), B, 0, st>>>(NPR, flag, rid, P->pair_l, P->pair_r,
+                                                        P->run_l, P->run_r, run_start);
+            DPV_CHECK_LAUNCH();
+            k_run_len<<<grid_for(nr, B), B, 0, st>>>(nr, NPR, run_start, P->run_len);
+            DPV_CHECK_LAUNCH();
+        }
+        k_key_runs<<<grid_for(W + 1, B), B, 0, st>>>(W, P->key_pair_ptr, rid, P->key_run_ptr);
+        DPV_CHECK_LAUNCH();
     }
 
     // 11. key -> segment CSR (pose blocks) and var -> segment CSR (rhs_pose)

@@ -101,6 +101,11 @@ struct dpv_problem {
     int64_t* key_pair_ptr = nullptr;  // (W+1)
     int32_t* pair_l = nullptr;     // (NP) incidence index (left)
     int32_t* pair_r = nullptr;     // (NP) incidence index (right)
+    int64_t NR = 0;                // pair runs
+    int32_t* key_run_ptr = nullptr;   // (W+1) runs per key
+    int32_t* run_l = nullptr;      // (NR) first left incidence of the run
+    int32_t* run_r = nullptr;      // (NR) first right incidence
+    int32_t* run_len = nullptr;    // (NR) pairs in the run
     int32_t* key_seg_ptr = nullptr;   // (W+1)
     int32_t* key_seg = nullptr;    // (KS) seg*2 + (negative)
     int32_t* var_seg_ptr = nullptr;   // (n+1)
@@ -194,6 +199,9 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
 int32_t coords(dpv_problem* p, const double* q, const double* t, const double* d, double scale,
                double* out, cudaStream_t st);
 int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cudaStream_t st);
+int32_t coords_sel(dpv_problem* p, const double* q, const double* t, const double* d,
+                   double scale, const int64_t* sel, int64_t n_sel, double* out,
+                   cudaStream_t st);
 int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
                        cudaStream_t st);
 int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,

@@ -53,6 +53,26 @@ def test_corr_matches_oracle(dtype):
         assert np.allclose(pyr[1].cpu().numpy(), corr_oracle.avg_pool4(f), atol=1e-6)
 
 
+@pytest.mark.parametrize("E,C", [(3000, 128), (2000, 64), (1500, 256)])
+def test_corr_bf16_tensor_core_pipeline(E, C):
+    """Several items per CTA (double-buffered staging) and every channel
+    count with a tensor-core instantiation, against the oracle on the same
+    bf16 values."""
+    rng = np.random.default_rng(E + C)
+    g, f, coords, ii, jj = make(rng, E=E, C=C, F=6, H=24, W=32, P=80)
+    coords[5::97, :, 1] = np.linspace(0, 40, 9)      # some wide windows (fallback)
+    gd = torch.as_tensor(g, device="cuda").to(torch.bfloat16)
+    fd = torch.as_tensor(f, device="cuda").to(torch.bfloat16)
+    pyr = corr.pyramid(fd)
+    out = corr.corr(gd, pyr, torch.as_tensor(coords, device="cuda"),
+                    torch.as_tensor(ii, device="cuda"), torch.as_tensor(jj, device="cuda"))
+    ref = corr_oracle.corr(gd.double().cpu().numpy(),
+                           [fd.double().cpu().numpy(), pyr[1].double().cpu().numpy()],
+                           coords, ii, jj)
+    err = np.abs(out.cpu().numpy() - ref).max()
+    assert err < 2e-4 * np.sqrt(C / 128), err
+
+
 def test_corr_on_reprojected_patches():
     """K2 -> K1: correlation at the BA problem's reprojections peaks at the
     center when the features of frame j are those sampled from the truth."""
