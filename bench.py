@@ -202,6 +202,7 @@ class Stepper:
         dev = "cuda"
         self.Ec = len(work["csel"])
         self.side = torch.cuda.Stream()           # K1 runs beside the BA step
+        self.overlap = True                       # False: serialise (per-kernel timing)
         self.ev_fork = torch.cuda.Event()
         self.ev_join = torch.cuda.Event()
         self.coords = torch.empty((self.Ec, 9, 2), dtype=torch.float64, device=dev)
@@ -228,8 +229,9 @@ class Stepper:
         # K2 pixels of the correlation edges -> K1, on a side stream: the
         # correlation is independent of this BA step and overlaps it
         self.ev_fork.record()
-        with torch.cuda.stream(self.side):
-            self.side.wait_event(self.ev_fork)
+        side = self.side if self.overlap else torch.cuda.current_stream()
+        with torch.cuda.stream(side):
+            side.wait_event(self.ev_fork)
             L.check(lib.dpv_reproject_coords_sel(self.h, P(q), P(t), P(d), 0.25, P(w["csel"]),
                                                  self.Ec, P(self.coords), L.stream_ptr()),
                     "coords")
@@ -279,37 +281,52 @@ def cholesky_flops(N, nb=64):
     return syrk, other
 
 
+def load_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed `ncu --set full` capture (profiles/ncu_traffic.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
+
+
 def kernel_rooflines(timing, work, steps, hbm_peak):
+    """Per-kernel roofline: ALGORITHMIC bytes (or FP64 flops) per launch over
+    the CUDA-event launch time (DESIGN.md section 4 gives the per-unit figures)."""
     E = work["E_local"]     # this rank's edges (= E at N = 1)
     info = work["info"]
     P = int(info.n_depths)
     n = int(info.n_free)
-    N = 6 * n
+    W = int(info.n_keys)
+    I = int(info.n_inc)
     Ec = len(work["csel"])
     L = len(work["pyr"])
     fbytes = 2 if work["gmap"].dtype.itemsize == 2 else 4
-    syrk_flops, _ = cholesky_flops(N)
-    plan = work.get("plan")
-    if plan is not None:        # sparse tile plan: only the planned update tiles
-        syrk_flops = plan["update_flops"]
+    plan = work.get("plan") or {}
+    traffic = load_traffic()
+    edge_pass = E * 172 + P * 152      # targets, weights, indices + per-row rays/depth
     out = {}
     per_step = {
         # name: (bound, algorithmic bytes or flops per step, unit)
-        "assemble_edges": ("fp64+hbm", E * 172 + P * 152, "B"),
-        "objective": ("hbm", E * 172 + P * 152, "B"),
+        "assemble_edges": ("hbm", edge_pass + E * 64 + int(info.n_segments) * 216, "B"),
+        "objective": ("hbm", edge_pass, "B"),
         # corr edges: src/dst/row (12) + the patch's rays and depth (152) in, 144 out
         "coords": ("hbm", Ec * (12 + 152 + 144), "B"),
-        "syrk": ("tensor", syrk_flops, "flop"),
         # coords + indices + output + the edges' patch features + every feature map once
         "corr": ("hbm", Ec * (144 + 8 + L * 9 * 49 * 4) + Ec * 9 * work["C"] * fbytes
                  + sum(int(f.numel()) * fbytes for f in work["pyr"]), "B"),
-        "key_blocks": ("fp64", int(info.n_pairs) * 72.0, "flop"),
-        # 64x64 factor (64^3/3 FMA) + inverse (64^3/3 FMA) per panel, one CTA
-        "potrf_inv": ("latency", 2.0 * (2 * 64 ** 3 / 3) * ((N + 63) // 64), "flop"),
+        # per-row sums: e_terms (c_dd, g_d) of every edge in, 4 row arrays out
+        "rows": ("hbm", E * (4 + 16) + P * 25, "B"),
+        # +-e_pd of every contribution in, inc_block + uinc out
+        "incidences": ("hbm", 2 * E * (4 + 48) + I * 96, "B"),
+        # Schur pair products on DMMA: 72 flop per pair (6x6 outer product)
+        "key_blocks": ("tensor", int(info.n_pairs) * 72.0, "flop"),
+        # band+border factorisation on DMMA (the plan's tile products)
+        "spd_factor": ("tensor", plan.get("update_flops", 0.0), "flop"),
     }
     for name, (ms, cnt) in timing.items():
         rec = {"ms_per_step": ms / steps, "launches_per_step": cnt / steps}
-        if name in per_step:
+        if name in per_step and per_step[name][1] > 0:
             bound, work_units, unit = per_step[name]
             per_launch = work_units / max(cnt / steps, 1)
             avg_ms = ms / max(cnt, 1)
@@ -321,6 +338,7 @@ def kernel_rooflines(timing, work, steps, hbm_peak):
                 ach = per_launch / (avg_ms * 1e-3) / 1e12
                 rec.update(bound=bound, achieved=ach, unit="TFLOP/s", peak=FP64_DMMA_PEAK,
                            frac=ach / FP64_DMMA_PEAK, algorithmic_per_launch=per_launch)
+            rec["traffic"] = traffic.get(name)
         out[name] = rec
     return out
 
@@ -414,30 +432,42 @@ def run_ours(args):
         ms_per_step = float(mt.item())
     value = work["E"] / (ms_per_step * 1e-3)
     # per-kernel CUDA-event timing pass (separate, so the headline has no event overhead)
+    # per-kernel CUDA-event pass: the correlation runs on the main stream here,
+    # so every kernel is timed alone (the headline overlaps it with the BA)
+    st.overlap = False
     _lib.timing_enable(True)
     for _ in range(args.steps):
         st.step()
     timing = _lib.timing_collect()
     _lib.timing_enable(False)
+    st.overlap = True
     try:
         work["plan"] = _lib.plan_info(work["prob"]._ensure())
     except Exception:
         work["plan"] = None
     kernels = kernel_rooflines(timing, work, args.steps, hbm_peak)
-    dominant = max(kernels.items(), key=lambda kv: kv[1]["ms_per_step"])
+    # dominant kernel = largest share of the (serialised) step
+    dominant = max(((k, v) for k, v in kernels.items() if "bound" in v),
+                   key=lambda kv: kv[1]["ms_per_step"])
     dom = dict(dominant[1])
-    bound = dom.get("bound", "hbm")
-    roof = {"kernel": dominant[0],
-            "bound": {"fp64": "fp64", "fp64+hbm": "fp64", "latency": "latency"}.get(bound, bound),
+    roof = {"kernel": dominant[0], "bound": dom["bound"],
             "achieved": dom.get("achieved"), "peak": dom.get("peak"),
-            "unit": dom.get("unit"), "frac": dom.get("frac"), "traffic": None,
+            "unit": dom.get("unit"), "frac": dom.get("frac"), "traffic": dom.get("traffic"),
             "share_of_step": dom["ms_per_step"] / ms_per_step,
-            "peak_source": ("FP64 peak measured on this pool (DMMA 37.18 / DFMA 36.86 TFLOP/s, "
-                            "profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure")
-            if dom.get("unit") == "TFLOP/s" else "MEASURED_PEAKS.json hbm_gbs"}
-    if roof["bound"] == "latency":
-        roof["note"] = ("critical-path diagonal-block factorisation (one CTA per 64-column panel, "
-                        "188 in sequence); see `kernels` for the bandwidth / tensor kernels")
+            "peak_source": ("FP64 DMMA peak measured on this pool (37.18 TFLOP/s, "
+                            "profiles/fp64_peak_r01.txt; MEASURED_PEAKS.json has no FP64 "
+                            "figure)") if dom.get("unit") == "TFLOP/s"
+            else "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+    notes = {
+        "spd_factor": "latency-bound dataflow chain (leader CTA per chain: 64x64 potrf + TRSM "
+                      "+ diagonal update per panel); tensor frac is low by construction",
+        "assemble_edges": "FP64-pipe bound (~1.3k FP64 ops per 172-byte edge, SURVEY H1)",
+        "key_blocks": "L2-gather bound DMMA Schur products",
+    }
+    if dominant[0] in notes:
+        roof["note"] = notes[dominant[0]]
+    serial_ms = sum(v["ms_per_step"] for v in kernels.values())
+    roof["serialised_kernel_ms"] = serial_ms
 
     # e2e through the C-ABI from pinned host buffers
     e2e = None
@@ -494,8 +524,11 @@ def run_ours(args):
 
 
 def run_e2e(work, st, args, torch):
-    """Host buffers -> C-ABI -> host: per step H2D flow targets + confidences
-    (all BA edges) + state, the device step, D2H of the candidate state."""
+    """Host buffers -> C-ABI -> host: per step H2D of the flow targets +
+    confidences (all BA edges) + state, the device step, D2H of the candidate
+    state and objective.  Uploads are double-buffered on a copy stream, so
+    step i+1's inputs cross PCIe while step i computes (whole-job throughput);
+    every step's copies are inside the timed region."""
     from paper_2408_01654_b200 import _lib
     prob = work["prob"]
     E = work["E"]
@@ -506,34 +539,63 @@ def run_e2e(work, st, args, torch):
     q_h = work["q"].cpu().pin_memory()
     t_h = work["t"].cpu().pin_memory()
     d_h = work["d"].cpu().pin_memory()
-    tgt_d = torch.empty_like(tgt_h, device="cuda")
-    conf_d = torch.empty_like(conf_h, device="cuda")
-    q_d, t_d, d_d = (torch.empty_like(x, device="cuda") for x in (q_h, t_h, d_h))
+    host_in = (tgt_h, conf_h, q_h, t_h, d_h)
+    bufs = [[torch.empty_like(x, device="cuda") for x in host_in] for _ in range(2)]
     outs = [torch.empty_like(x).pin_memory() for x in (q_h, t_h, d_h)]
     obj_h = torch.empty(1, dtype=torch.float64).pin_memory()
     lib = _lib.lib()
+    copy = torch.cuda.Stream()
+    loaded = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    main = torch.cuda.current_stream()
+    for ev in consumed:
+        ev.record(main)
 
-    def step():
-        tgt_d.copy_(tgt_h, non_blocking=True)
-        conf_d.copy_(conf_h, non_blocking=True)
-        q_d.copy_(q_h, non_blocking=True)
-        t_d.copy_(t_h, non_blocking=True)
-        d_d.copy_(d_h, non_blocking=True)
+    def upload(i):
+        b = i % 2
+        with torch.cuda.stream(copy):
+            copy.wait_event(consumed[b])
+            for dst, src in zip(bufs[b], host_in):
+                dst.copy_(src, non_blocking=True)
+            loaded[b].record(copy)
+
+    def step(i, last):
+        b = i % 2
+        if not last:
+            upload(i + 1)                      # next step's inputs, overlapped
+        main.wait_event(loaded[b])
+        tgt_d, conf_d, q_d, t_d, d_d = bufs[b]
         _lib.check(lib.dpv_update_targets(st.h, _lib.ptr(tgt_d), _lib.ptr(conf_d),
                                           _lib.stream_ptr()), "update_targets")
         st.step(q_d, t_d, d_d)
+        consumed[b].record(main)
         outs[0].copy_(st.q2, non_blocking=True)
         outs[1].copy_(st.t2, non_blocking=True)
         outs[2].copy_(st.d2, non_blocking=True)
         obj_h.copy_(st.obj, non_blocking=True)
 
-    for _ in range(2):
-        step()
-    ms = time_steps(step, max(2, args.steps // 2), torch) / max(2, args.steps // 2)
-    h2d = sum(int(x.numel() * x.element_size()) for x in (tgt_h, conf_h, q_h, t_h, d_h))
+    def run(k):
+        upload(0)
+        for i in range(k):
+            step(i, i == k - 1)
+
+    run(2)
+    K = max(2, args.steps)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    run(K)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / K
+    h2d = sum(int(x.numel() * x.element_size()) for x in host_in)
     d2h = sum(int(x.numel() * x.element_size()) for x in outs) + 8
     return {"value": E / (ms * 1e-3), "unit": "patch-edges/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "h2d_GBps": h2d / (ms * 1e-3) / 1e9,
+            "note": "uploads double-buffered on a copy stream (PCIe-bound: the f64 flow "
+                    "targets of every BA edge cross each step)"}
 
 
 def run_global(work, args, torch):
