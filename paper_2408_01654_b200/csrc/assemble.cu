@@ -6,6 +6,8 @@
 // (ba.py:328-440) with geometry.reproject_grid (geometry.py:478-529) inlined.
 // Every reduction runs over a fixed, index-sorted list (no float atomics), so
 // results are bit-identical run to run.
+#include <cstdlib>
+
 #include "problem.cuh"
 
 namespace dpv {
@@ -126,8 +128,8 @@ __global__ void __launch_bounds__(256) k_objective(
 
 // same sum, one warp per (src, dst) segment: the two frames are loaded once
 // per segment into shared memory, lanes stride over the segment's edges.
-template <int M>
-__global__ void __launch_bounds__(256) k_objective_seg(
+template <int M, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_objective_seg(
     int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
     const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
     const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(256) k_objective_seg(
             const double id = __drcp_rn(__ldg(d + row));
             const double w0 = a_w[e], w1 = a_w[E + e];
             double sum = 0.0;
-#pragma unroll
+#pragma unroll U
             for (int c = 0; c < M; ++c) {
                 Cell cl;
                 reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
@@ -297,8 +299,9 @@ __device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
     return a * 6 - (a * (a - 1)) / 2 + (b - a);
 }
 
-__global__ void __launch_bounds__(128, 3) k_assemble_edges(
-    int64_t S, int64_t E, int m, int64_t P, const int32_t* __restrict__ seg_ptr,
+template <int M, int U, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_assemble_edges(
+    int64_t S, int64_t E, int m_unused, int64_t P, const int32_t* __restrict__ seg_ptr,
     const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
     const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
     const double* __restrict__ a_w, const double* __restrict__ r_ray,
@@ -335,7 +338,8 @@ __global__ void __launch_bounds__(128, 3) k_assemble_edges(
             const double sw0 = sqrt(a_w[e]), sw1 = sqrt(a_w[E + e]);
             double ep[6] = {0, 0, 0, 0, 0, 0};
             double cdd = 0.0, gd = 0.0;
-            for (int c = 0; c < m; ++c) {
+#pragma unroll U
+            for (int c = 0; c < M; ++c) {
                 Cell cl;
                 reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
                                __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr,
@@ -604,10 +608,25 @@ int32_t objective(dpv_problem* p, const double* q, const double* t, const double
     DPV_TRY(frame_rotations(p, q, st));
     DPV_TSTART("objective", st);
     if (p->m == 9 && p->S > 0)
-        k_objective_seg<9><<<kObjBlocks, 256, 0, st>>>(
-            p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,
-            p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
-            p->obj_part);
+    {
+        const int variant = getenv("DPV_OBJ_VARIANT") ? atoi(getenv("DPV_OBJ_VARIANT")) : 0;
+#define DPV_OBJ(U, B)                                                                        \
+    k_objective_seg<9, U, B><<<kObjBlocks, 256, 0, st>>>(                                    \
+        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,    \
+        p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3], p->obj_part)
+        switch (variant) {
+            case 1: DPV_OBJ(1, 4); break;
+            case 2: DPV_OBJ(3, 3); break;
+            case 3: DPV_OBJ(9, 3); break;
+            case 4: DPV_OBJ(1, 3); break;
+            case 5: DPV_OBJ(2, 4); break;
+            case 6: DPV_OBJ(3, 4); break;
+            case 7: DPV_OBJ(1, 5); break;
+            case 8: DPV_OBJ(9, 2); break;
+            default: DPV_OBJ(3, 4); break;
+        }
+#undef DPV_OBJ
+    }
     else
         k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
                                                 p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d,
@@ -675,14 +694,26 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     auto* grad_bits = reinterpret_cast<unsigned long long*>(p->scal);
     auto* n_inactive = reinterpret_cast<unsigned long long*>(p->scal + 6);
     if (p->S > 0) {
+        DPV_ARG(p->m == 9, "assembly kernel is instantiated for 3x3 patches");
         const int warps_per_block = 4;
         int blocks = (int)std::min<int64_t>((p->S + warps_per_block - 1) / warps_per_block,
                                             (int64_t)sm_count() * 64);
         DPV_TSTART("assemble_edges", st);
-        k_assemble_edges<<<blocks, 32 * warps_per_block, 0, st>>>(
-            p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,
-            p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
-            p->e_terms, p->seg_h, p->seg_g);
+        const int variant = getenv("DPV_ASM_VARIANT") ? atoi(getenv("DPV_ASM_VARIANT")) : 0;
+#define DPV_ASM(U, B)                                                                          \
+    k_assemble_edges<9, U, B><<<blocks, 32 * warps_per_block, 0, st>>>(                        \
+        p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,        \
+        p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
+        p->e_terms, p->seg_h, p->seg_g)
+        switch (variant) {
+            case 1: DPV_ASM(1, 4); break;
+            case 2: DPV_ASM(1, 3); break;
+            case 3: DPV_ASM(2, 3); break;
+            case 4: DPV_ASM(1, 2); break;
+            case 5: DPV_ASM(3, 2); break;
+            default: DPV_ASM(3, 3); break;
+        }
+#undef DPV_ASM
         DPV_CHECK_LAUNCH();
     }
     if (p->P > 0) {
