@@ -675,7 +675,7 @@ int32_t dpv_block_sparse_solve(const int64_t* keys, int64_t n_keys, int64_t n,
         kb[w] = (int32_t)b;
     }
     SpdPlan* plan = nullptr;
-    DPV_TRY(spd_plan_build(ka.data(), kb.data(), n_keys, n, &plan));
+    DPV_TRY(spd_plan_build(ka.data(), kb.data(), n_keys, n, &plan, st));
     int32_t* dk = nullptr;
     cudaError_t e = cudaMallocAsync(&dk, sizeof(int32_t) * 2 * n_keys, st);
     int32_t rc = DPV_OK;

@@ -30,7 +30,8 @@ int32_t build_factor_plan(int64_t N, const std::vector<char>* tile_pattern, Fact
 
 // Banded + border sparse SPD solver of the reduced camera system (spd.cu).
 struct SpdPlan;
-int32_t spd_plan_build(const int32_t* ka, const int32_t* kb, int64_t W, int64_t n, SpdPlan** out);
+int32_t spd_plan_build(const int32_t* ka, const int32_t* kb, int64_t W, int64_t n, SpdPlan** out,
+                       cudaStream_t st);
 void spd_plan_free(SpdPlan* p);
 int64_t spd_plan_bytes(const SpdPlan* p);
 void spd_plan_describe(const SpdPlan* p, int64_t* v);

@@ -432,7 +432,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
             DPV_CUDA(cudaMemcpyAsync(kb.data(), p->key_b, sizeof(int32_t) * p->W,
                                      cudaMemcpyDeviceToHost, st));
             DPV_CUDA(cudaStreamSynchronize(st));
-            DPV_TRY(spd_plan_build(ka.data(), kb.data(), p->W, p->n, &p->spd));
+            DPV_TRY(spd_plan_build(ka.data(), kb.data(), p->W, p->n, &p->spd, st));
             DPV_TRY(p->alloc(&p->sblk, p->W * 36));
         }
         DPV_TRY(reduced_system(p, lam, p->sblk, p->red_rhs, nullptr, st));
