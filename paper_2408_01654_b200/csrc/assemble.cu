@@ -481,7 +481,8 @@ __device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, doubl
 
 // pose blocks (ba.py:389-394) and Schur blocks E C0^-1 E^T (ba.py:405-413):
 // one warp per union key, fixed lane-strided order + xor-tree reduction
-__global__ void __launch_bounds__(128) k_key_blocks(
+template <int UNR, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_key_blocks(
     int64_t W, const int32_t* key_seg_ptr, const int32_t* key_seg, const double* seg_h,
     const int32_t* __restrict__ key_run_ptr, const int32_t* __restrict__ run_l,
     const int32_t* __restrict__ run_r, const int32_t* __restrict__ run_len,
@@ -523,18 +524,18 @@ __global__ void __launch_bounds__(128) k_key_blocks(
             const int32_t len = run_len[q];
             const double* ub = uinc + (int64_t)run_l[q] * 6;
             const double* vb = inc_block + (int64_t)run_r[q] * 6;
-            // 8 steps (32 pairs) of loads in flight, then 8 DMMAs
-            for (int32_t t0 = 0; t0 < len; t0 += 32) {
-                double a[8], b[8];
+            // UNR steps (4*UNR pairs) of loads in flight, then UNR DMMAs
+            for (int32_t t0 = 0; t0 < len; t0 += 4 * UNR) {
+                double a[UNR], b[UNR];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < UNR; ++u) {
                     const int32_t t = t0 + 4 * u + kq;
                     const bool ok = t < len && ci < 6;
                     a[u] = ok ? __ldg(ub + (int64_t)t * 6 + ci) : 0.0;
                     b[u] = ok ? __ldg(vb + (int64_t)t * 6 + ci) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) dmma_f64(c[u & 3][0], c[u & 3][1], a[u], b[u]);
+                for (int u = 0; u < UNR; ++u) dmma_f64(c[u & 3][0], c[u & 3][1], a[u], b[u]);
             }
         }
         // C[i][j] at lane (i = lane>>2, j = 2*(lane&3) + h)
@@ -733,10 +734,22 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     if (p->W > 0) {
         int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("key_blocks", st);
-        k_key_blocks<<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
-                                             p->key_run_ptr, p->run_l, p->run_r, p->run_len,
-                                             p->uinc, p->inc_block, p->pose_blocks,
-                                             p->schur_blocks);
+        const int kv = getenv("DPV_KEY_VARIANT") ? atoi(getenv("DPV_KEY_VARIANT")) : 0;
+#define DPV_KEY(U, B)                                                                          \
+    k_key_blocks<U, B><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,     \
+                                               p->key_run_ptr, p->run_l, p->run_r, p->run_len, \
+                                               p->uinc, p->inc_block, p->pose_blocks,          \
+                                               p->schur_blocks)
+        switch (kv) {
+            case 1: DPV_KEY(8, 1); break;
+            case 2: DPV_KEY(16, 1); break;
+            case 3: DPV_KEY(16, 3); break;
+            case 4: DPV_KEY(24, 2); break;
+            case 5: DPV_KEY(32, 2); break;
+            case 6: DPV_KEY(8, 4); break;
+            default: DPV_KEY(16, 3); break;
+        }
+#undef DPV_KEY
         DPV_CHECK_LAUNCH();
     }
     if (p->n > 0) {

@@ -32,7 +32,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--variants", default="0")
-    ap.add_argument("--asm-variants", default="0,1,2,3,4,5")
+    ap.add_argument("--asm-variants", default="0")
+    ap.add_argument("--key-variants", default="0,1,2,3,4")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     t0 = time.time()
@@ -60,6 +61,14 @@ def main():
         _lib.timing_enable(False)
         ae = tm.get("assemble_edges", (0, 1))
         print(f"assemble variant {v}: chain {ms:.3f} ms, k_assemble_edges {ae[0] / ae[1]:.3f} ms")
+    for v in a.key_variants.split(","):
+        os.environ["DPV_KEY_VARIANT"] = v
+        _lib.timing_enable(True)
+        ms = timeit(lambda: lib.dpv_assemble(h, P(q), P(t), P(d), s()))
+        tm = _lib.timing_collect()
+        _lib.timing_enable(False)
+        kb = tm.get("key_blocks", (0, 1))
+        print(f"key variant {v}: chain {ms:.3f} ms, k_key_blocks {kb[0] / kb[1]:.3f} ms")
 
 
 if __name__ == "__main__":
