@@ -335,7 +335,8 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
             const int32_t row = a_row[e];
             const double dd = __ldg(d + row);
             const double id = __drcp_rn(dd);
-            const double sw0 = sqrt(a_w[e]), sw1 = sqrt(a_w[E + e]);
+            // w J^T J instead of (sqrt(w) J)^T (sqrt(w) J) (ba.py:355-366): no sqrt
+            const double w0 = a_w[e], w1 = a_w[E + e];
             double ep[6] = {0, 0, 0, 0, 0, 0};
             double cdd = 0.0, gd = 0.0;
 #pragma unroll U
@@ -344,8 +345,6 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
                 reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
                                __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr,
                                cl);
-                const double s0 = cl.valid ? sw0 : 0.0;
-                const double s1 = cl.valid ? sw1 : 0.0;
                 const double iz = cl.iz;
                 // A = Jproj R_j^T (geometry.py:514-522)
                 const double p0 = intr[0] * iz, q0 = -intr[0] * cl.xt[0] * iz * iz;
@@ -370,23 +369,22 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
                 for (int r = 0; r < 2; ++r) jd[r] = J[r][0] * g0 + J[r][1] * g1 + J[r][2] * g2;
                 const double rr[2] = {(cl.u - a_tgt[(int64_t)(2 * c) * E + e]) ,
                                       (cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e])};
-                const double sw[2] = {s0, s1};
+                const double wv[2] = {cl.valid ? w0 : 0.0, cl.valid ? w1 : 0.0};
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    double jw[6];
+                    double wj[6];
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) jw[k] = J[r][k] * sw[r];
-                    const double jdw = jd[r] * sw[r];
-                    const double rw = rr[r] * sw[r];
+                    for (int k = 0; k < 6; ++k) wj[k] = J[r][k] * wv[r];
+                    const double wjd = jd[r] * wv[r];
 #pragma unroll
                     for (int a = 0; a < 6; ++a) {
 #pragma unroll
-                        for (int b = a; b < 6; ++b) H[utri(a, b)] += jw[a] * jw[b];
-                        G[a] += jw[a] * rw;
-                        ep[a] += jw[a] * jdw;
+                        for (int b = a; b < 6; ++b) H[utri(a, b)] += wj[a] * J[r][b];
+                        G[a] += wj[a] * rr[r];
+                        ep[a] += wj[a] * jd[r];
                     }
-                    cdd += jdw * jdw;
-                    gd += jdw * rw;
+                    cdd += wjd * jd[r];
+                    gd += wjd * rr[r];
                 }
             }
 #pragma unroll
