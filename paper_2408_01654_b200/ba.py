@@ -510,9 +510,10 @@ def solve_dense(system: BlockSparseSystem, lam: float | None = None):
 
 def solve_block_sparse(system: BlockSparseSystem, lam: float | None = None):
     """Block-sparse backend (ba.py:475-487).  Same numbers (the reduced system
-    is factorised by the dense FP64 tensor-core Cholesky; agreement with the
-    reference block Cholesky is 1e-8, test_ba.py:192-201); ``peak_block_count``
-    is the exact symbolic fill of the natural-order block factor."""
+    is factorised by the band + border sparse FP64 tensor-core factorisation,
+    spd.cu; agreement with the reference block Cholesky is 1e-8,
+    test_ba.py:192-201); ``peak_block_count`` is the exact symbolic fill of
+    the natural-order block factor."""
     lam = system.damping if lam is None else lam
     dp, dd, dt = _device_solve(system, lam)
     stats = {"backend": BLOCK_SPARSE, "factorize_s": dt, "solve_s": 0.0,

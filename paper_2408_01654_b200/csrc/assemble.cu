@@ -388,9 +388,12 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 6; ++k) e_terms[(int64_t)k * E + e] = ep[k];
-            e_terms[6 * E + e] = cdd;
-            e_terms[7 * E + e] = gd;
+            // AoS (E, 8): the row / incidence gathers read one 64-byte record
+            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
+            et[0] = make_double2(ep[0], ep[1]);
+            et[1] = make_double2(ep[2], ep[3]);
+            et[2] = make_double2(ep[4], ep[5]);
+            et[3] = make_double2(cdd, gd);
         }
 #pragma unroll
         for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
@@ -423,8 +426,9 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
         double c = 0.0, g = 0.0;
         for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
             const int32_t e = row_pos[k];
-            c += e_terms[6 * E + e];
-            g += e_terms[7 * E + e];
+            const double2 cg = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)e * 8 + 6));
+            c += cg.x;
+            g += cg.y;
         }
         depth_diag[r] = c;
         rhs_depth[r] = -g;
@@ -459,8 +463,13 @@ __global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const
             const int32_t code = inc_con[k];
             const int32_t e = code >> 1;
             const double sgn = (code & 1) ? -1.0 : 1.0;
+            const double2* et = reinterpret_cast<const double2*>(e_terms + (int64_t)e * 8);
 #pragma unroll
-            for (int a = 0; a < 6; ++a) acc[a] += sgn * e_terms[(int64_t)a * E + e];
+            for (int a = 0; a < 3; ++a) {
+                const double2 v = __ldg(et + a);
+                acc[2 * a] += sgn * v.x;
+                acc[2 * a + 1] += sgn * v.y;
+            }
         }
         const double c = cinv0[inc_row[i]];
 #pragma unroll

@@ -117,7 +117,7 @@ struct dpv_problem {
 
     // ---- assembled system -----------------------------------------------------
     double* frame_R = nullptr;     // (F, 9)
-    double* e_terms = nullptr;     // (8, E): e_pd[6], c_dd, g_d
+    double* e_terms = nullptr;     // (E, 8): e_pd[6], c_dd, g_d
     double* seg_h = nullptr;       // (S, 21) upper-triangular sum of J^T W J
     double* seg_g = nullptr;       // (S, 6)  sum of J^T W r
     double* depth_diag = nullptr;  // (P)

@@ -353,6 +353,22 @@ CONFIGS = {
                            look="inward", image_size=(640, 480),
                            intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0), extent=250.0),
                  loops=2000, free=lambda n: (1, n - 1)),
+    # KITTI shape: forward-looking square loop, 4500 frames
+    "cfg4": dict(spec=dict(kind="square-loop", n_frames=4500, seed=0, n_landmarks=324000,
+                           look="forward", image_size=(1226, 370),
+                           intrinsics=Intrinsics(718.856, 718.856, 607.193, 185.216),
+                           extent=440.0),
+                 loops=4500, free=lambda n: (1, n - 1)),
+}
+
+DESCRIPTIONS = {
+    "cfg1": "16-frame local window (circle, 96 patches/frame, radius 13)",
+    "cfg2": "EuRoC-shape 22-frame window (752x480, 96 patches/frame, radius 13)",
+    "mid": "120-frame loop graph (circle, 96 patches/frame, radius 13, loop edges)",
+    "cfg3": "2000-frame global loop-closure BA (circle, 96 patches/frame, radius 13, "
+            "33x32 loop edges)",
+    "cfg4": "KITTI-shape 4500-frame global BA (1226x370, forward square loop, 96 patches/frame, "
+            "radius 13, 75x32 loop edges)",
 }
 
 
