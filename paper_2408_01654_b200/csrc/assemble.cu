@@ -453,9 +453,11 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
 }
 
 // coupling blocks per (var, row) incidence (ba.py:397-403)
+// uinc = inc_block * cinv0[row] (pair kernel) or, grouped, the symmetric
+// factor w = inc_block * sqrt(cinv0[row]) so the Schur blocks are sums of w w^T
 __global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const int32_t* inc_con,
                              const int32_t* inc_row, const double* e_terms, const double* cinv0,
-                             double* inc_block, double* uinc) {
+                             double* inc_block, double* uinc, int sym) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I;
          i += (int64_t)gridDim.x * blockDim.x) {
         double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -471,7 +473,8 @@ __global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const
                 acc[2 * a + 1] += sgn * v.y;
             }
         }
-        const double c = cinv0[inc_row[i]];
+        const double c0 = cinv0[inc_row[i]];
+        const double c = sym ? sqrt(c0) : c0;
 #pragma unroll
         for (int a = 0; a < 6; ++a) {
             inc_block[i * 6 + a] = acc[a];
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(128, MINB) k_key_blocks(
     const int32_t* __restrict__ key_run_ptr, const int32_t* __restrict__ run_l,
     const int32_t* __restrict__ run_r, const int32_t* __restrict__ run_len,
     const double* __restrict__ uinc, const double* __restrict__ inc_block,
-    double* __restrict__ pose_blocks, double* __restrict__ schur_blocks) {
+    double* __restrict__ pose_blocks, double* __restrict__ schur_blocks, int pose_only) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -520,6 +523,7 @@ __global__ void __launch_bounds__(128, MINB) k_key_blocks(
             for (int q = 0; q < 21; ++q) v = (q == t) ? h[q] : v;
             pose_blocks[w * 36 + idx] = v;
         }
+        if (pose_only) continue;
         // Schur block = U^T V over the key's pair runs (l+t, r+t) on the FP64
         // tensor cores: per m8n8k4 step 4 pairs; lane (k = lane&3, i = lane>>2)
         // loads component i of pair k of both sides, so a quad reads 4
@@ -556,11 +560,112 @@ __global__ void __launch_bounds__(128, MINB) k_key_blocks(
     }
 }
 
+// Grouped Schur complement: per chunk of rows sharing one incidence-var list
+// (v_0 < ... < v_{m-1}), stage W (6m x nr: var j's 6 components on rows
+// 6j..6j+5, columns = rows of the chunk) in shared memory and form the upper
+// triangle of W W^T on DMMA (m8n8k4, K = rows) over 8x8 tiles of the packed
+// 6m rows; every element lands in its 6x6 var block (j1 <= j2), the chunk's
+// contribution to schur_blocks[key(v_j1, v_j2)] (ba.py:405-413).
+__global__ void __launch_bounds__(256) k_group_syrk(const int4* __restrict__ chunks,
+                                                     const int32_t* __restrict__ rows,
+                                                     const int32_t* __restrict__ rinc_ptr,
+                                                     const int32_t* __restrict__ rinc,
+                                                     const double* __restrict__ w,
+                                                     double* __restrict__ sbuf) {
+    extern __shared__ double Ws[];
+    const int4 ch = chunks[blockIdx.x];
+    const int nr = ch.y, m = ch.z;
+    const int n6 = 6 * m, TR = (n6 + 7) / 8;
+    // K padded to the m8n8k4 step; row stride = 4 (mod 16) doubles
+    const int ldt = ((((nr + 3) & ~3) + 11) / 16) * 16 + 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int x = tid; x < m * ldt; x += blockDim.x) {
+        const int j = x / ldt, t = x % ldt;
+        double v[6] = {0, 0, 0, 0, 0, 0};
+        if (t < nr) {
+            const int32_t r = rows[ch.x + t];
+            const double2* src =
+                reinterpret_cast<const double2*>(w + (int64_t)rinc[rinc_ptr[r] + j] * 6);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double2 u = __ldg(src + q);
+                v[2 * q] = u.x;
+                v[2 * q + 1] = u.y;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) Ws[(6 * j + c) * ldt + t] = v[c];
+    }
+    for (int x = tid; x < (8 * TR - n6) * ldt; x += blockDim.x) Ws[n6 * ldt + x] = 0.0;
+    __syncthreads();
+    const int nt = TR * (TR + 1) / 2;
+    const int lr = lane >> 2, lc = lane & 3;
+    const int kend = (nr + 3) & ~3;
+    for (int q0 = warp * 2; q0 < nt; q0 += 16) {
+        int tt[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            int q = min(q0 + u, nt - 1), t1 = 0;
+            while (q >= TR - t1) {
+                q -= TR - t1;
+                ++t1;
+            }
+            tt[u][0] = t1;
+            tt[u][1] = t1 + q;
+        }
+        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const double* a0 = Ws + (8 * tt[0][0] + lr) * ldt + lc;
+        const double* b0 = Ws + (8 * tt[0][1] + lr) * ldt + lc;
+        const double* a1 = Ws + (8 * tt[1][0] + lr) * ldt + lc;
+        const double* b1 = Ws + (8 * tt[1][1] + lr) * ldt + lc;
+#pragma unroll 4
+        for (int k = 0; k < kend; k += 4) {
+            dmma_f64(c[0][0], c[0][1], a0[k], b0[k]);
+            dmma_f64(c[1][0], c[1][1], a1[k], b1[k]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (q0 + u >= nt) break;
+            const int r = 8 * tt[u][0] + lr;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cc = 8 * tt[u][1] + 2 * lc + h;
+                if (r >= n6 || cc >= n6) continue;
+                const int vr = r / 6, vc = cc / 6, i = r % 6, jj = cc % 6;
+                if (vr > vc) continue;              // mirror of an element of this tile
+                const int blk = vr * m - vr * (vr - 1) / 2 + (vc - vr);
+                double* dst = sbuf + ((int64_t)ch.w + blk) * 36;
+                dst[i * 6 + jj] = c[u][h];
+                if (vr == vc) dst[jj * 6 + i] = c[u][h];   // symmetric diagonal block
+            }
+        }
+    }
+}
+
+// schur_blocks[key] = sum of the key's chunk blocks in chunk order (warp per key)
+__global__ void k_key_schur_sum(int64_t W, const int32_t* __restrict__ key_blk_ptr,
+                                const int32_t* __restrict__ key_blk,
+                                const double* __restrict__ sbuf, double* __restrict__ schur) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < W; k += nwarps) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int32_t q = key_blk_ptr[k]; q < key_blk_ptr[k + 1]; ++q) {
+            const double* b = sbuf + (int64_t)key_blk[q] * 36;
+            s0 += __ldg(b + lane);
+            if (lane < 4) s1 += __ldg(b + 32 + lane);
+        }
+        schur[k * 36 + lane] = s0;
+        if (lane < 4) schur[k * 36 + 32 + lane] = s1;
+    }
+}
+
 // rhs_pose (ba.py:375-380) and rhs_schur = E C0^-1 w (ba.py:415-417): warp per var
 __global__ void k_var_rhs(int64_t n, const int32_t* var_seg_ptr, const int32_t* var_seg,
                           const double* seg_g, const int32_t* var_inc_ptr, const int32_t* inc_row,
-                          const double* uinc, const double* rhs_depth, double* rhs_pose,
-                          double* rhs_schur, unsigned long long* grad_bits) {
+                          const double* inc_block, const double* cinv0, const double* rhs_depth,
+                          double* rhs_pose, double* rhs_schur, unsigned long long* grad_bits) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -573,9 +678,10 @@ __global__ void k_var_rhs(int64_t n, const int32_t* var_seg_ptr, const int32_t* 
             for (int a = 0; a < 6; ++a) g[a] += sgn * seg_g[(int64_t)(code >> 1) * 6 + a];
         }
         for (int32_t i = var_inc_ptr[v] + lane; i < var_inc_ptr[v + 1]; i += 32) {
-            const double r = rhs_depth[inc_row[i]];
+            const int32_t row = inc_row[i];
+            const double r = rhs_depth[row] * cinv0[row];
 #pragma unroll
-            for (int a = 0; a < 6; ++a) sc[a] += uinc[(int64_t)i * 6 + a] * r;
+            for (int a = 0; a < 6; ++a) sc[a] += inc_block[(int64_t)i * 6 + a] * r;
         }
 #pragma unroll
         for (int a = 0; a < 6; ++a) {
@@ -735,7 +841,7 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         DPV_TSTART("incidences", st);
         k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
                                                            p->inc_row, p->e_terms, p->cinv0,
-                                                           p->inc_block, p->uinc);
+                                                           p->inc_block, p->uinc, p->grouped);
         DPV_CHECK_LAUNCH();
     }
     if (p->W > 0) {
@@ -746,7 +852,7 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     k_key_blocks<U, B><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,     \
                                                p->key_run_ptr, p->run_l, p->run_r, p->run_len, \
                                                p->uinc, p->inc_block, p->pose_blocks,          \
-                                               p->schur_blocks)
+                                               p->schur_blocks, p->grouped)
         switch (kv) {
             case 1: DPV_KEY(8, 1); break;
             case 2: DPV_KEY(16, 1); break;
@@ -758,13 +864,26 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         }
 #undef DPV_KEY
         DPV_CHECK_LAUNCH();
+        if (p->grouped) {
+            static size_t cur = 0;
+            const size_t smem = sizeof(double) * kSyrkSmemDoubles + 2048;
+            DPV_TRY(ensure_smem(k_group_syrk, smem, cur));
+            DPV_TSTART("group_syrk", st);
+            k_group_syrk<<<(int)p->n_chunks, 256, smem, st>>>(p->g_chunks, p->g_rows, p->rinc_ptr,
+                                                              p->rinc, p->uinc, p->g_sbuf);
+            DPV_CHECK_LAUNCH();
+            DPV_TSTART("key_schur_sum", st);
+            k_key_schur_sum<<<grid_for(p->W * 32, 256), 256, 0, st>>>(
+                p->W, p->key_blk_ptr, p->key_blk, p->g_sbuf, p->schur_blocks);
+            DPV_CHECK_LAUNCH();
+        }
     }
     if (p->n > 0) {
         int blocks = (int)std::min<int64_t>((p->n + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("var_rhs", st);
         k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
-                                          p->var_inc_ptr, p->inc_row, p->uinc, p->rhs_depth,
-                                          p->rhs_pose, p->rhs_schur, grad_bits);
+                                          p->var_inc_ptr, p->inc_row, p->inc_block, p->cinv0,
+                                          p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
         DPV_CHECK_LAUNCH();
         if (p->scale_degenerate) {
             DPV_TSTART("pin", st);

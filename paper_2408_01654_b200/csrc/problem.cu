@@ -7,6 +7,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "problem.cuh"
@@ -330,6 +331,86 @@ __global__ void k_key_runs(int64_t W, const int64_t* key_pair_ptr, const int32_t
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= W;
          w += (int64_t)gridDim.x * blockDim.x)
         key_run_ptr[w] = rid[key_pair_ptr[w]];
+}
+
+// ---- grouped Schur index: rows with identical incidence-var lists ---------
+__global__ void k_row_hash(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
+                           const int32_t* inc_var, uint64_t* h, int32_t* idx) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t x = 1469598103934665603ull ^ (uint64_t)(rinc_ptr[r + 1] - rinc_ptr[r]);
+        for (int32_t k = rinc_ptr[r]; k < rinc_ptr[r + 1]; ++k) {
+            x ^= (uint64_t)(uint32_t)inc_var[rinc[k]] + 0x9e3779b97f4a7c15ull;
+            x *= 1099511628211ull;
+            x ^= x >> 29;
+        }
+        h[r] = x;
+        idx[r] = (int32_t)r;
+    }
+}
+
+__global__ void k_group_flags(int64_t P, const uint64_t* hs, int32_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || hs[i] != hs[i - 1]) ? 1 : 0;
+}
+
+// group start positions (in sorted order) and a full check that every row's
+// var list equals its group head's (hash collisions -> *bad)
+__global__ void k_group_verify(int64_t P, const int32_t* flag, const int32_t* gid,
+                               const int32_t* rows, const int32_t* rinc_ptr, const int32_t* rinc,
+                               const int32_t* inc_var, int32_t* gstart, int32_t* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (flag[i]) gstart[gid[i]] = (int32_t)i;
+}
+
+__global__ void k_group_verify2(int64_t P, const int32_t* gid, const int32_t* gstart,
+                                const int32_t* rows, const int32_t* rinc_ptr, const int32_t* rinc,
+                                const int32_t* inc_var, int32_t* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = rows[i], h = rows[gstart[gid[i]]];
+        const int32_t m = rinc_ptr[r + 1] - rinc_ptr[r];
+        bool ok = m == rinc_ptr[h + 1] - rinc_ptr[h];
+        for (int32_t j = 0; ok && j < m; ++j)
+            ok = inc_var[rinc[rinc_ptr[r] + j]] == inc_var[rinc[rinc_ptr[h] + j]];
+        if (!ok) atomicExch(bad, 1);
+    }
+}
+
+// per chunk (rows of one group) and local block (j1 <= j2): the union-key
+// index of (var_j1, var_j2) and the block's slot in the chunk buffer
+__global__ void k_chunk_contrib(int64_t n_chunks, const int4* chunks, const int32_t* rows,
+                                const int32_t* rinc_ptr, const int32_t* rinc,
+                                const int32_t* inc_var, const uint64_t* union_keys, int64_t W,
+                                int64_t nfree, uint64_t* ckey, int32_t* cblk) {
+    for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const int4 ch = chunks[c];
+        const int32_t head = rows[ch.x];
+        const int m = ch.z;
+        const int nb = m * (m + 1) / 2;
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            int j1 = 0, rem = q;
+            while (rem >= m - j1) {
+                rem -= m - j1;
+                ++j1;
+            }
+            const int j2 = j1 + rem;
+            const uint64_t a = (uint64_t)inc_var[rinc[rinc_ptr[head] + j1]];
+            const uint64_t b = (uint64_t)inc_var[rinc[rinc_ptr[head] + j2]];
+            const uint64_t key = a * (uint64_t)nfree + b;
+            const int64_t w = lower_bound_dev(union_keys, W, key);
+            ckey[(int64_t)ch.w + q] = (uint64_t)w;
+            cblk[(int64_t)ch.w + q] = ch.w + q;
+        }
+    }
+}
+
+__global__ void k_sub_one(int64_t n, int32_t* a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] -= 1;
 }
 
 __global__ void k_gather_i32(int64_t n, const int32_t* idx, const int32_t* src, int32_t* dst) {
@@ -894,6 +975,109 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         }
         k_key_runs<<<grid_for(W + 1, B), B, 0, st>>>(W, P->key_pair_ptr, rid, P->key_run_ptr);
         DPV_CHECK_LAUNCH();
+    }
+
+    // 10c. grouped Schur complement: depth rows with identical incidence-var
+    // lists (all patches of a frame on a banded graph) form a group whose
+    // Schur contribution is one SYRK W_g W_g^T on the tensor cores; chunks of
+    // <= rows_per_chunk rows; each key sums its chunk blocks in a fixed order
+    P->grouped = 0;
+    // Opt-in (DPV_SCHUR_GROUPED=1): at cfg3 the pair-run DMMA kernel is faster
+    // (0.51 vs 0.44 + 0.1 ms: the grouped form wastes 8x8 tile work on 6-wide
+    // var blocks and its staging is a gather); it wins for dense var sets.
+    if (NPD > 0 && getenv("DPV_SCHUR_GROUPED") && atoi(getenv("DPV_SCHUR_GROUPED")) != 0) {
+        uint64_t *rh, *rh_s;
+        int32_t *ridx, *flag, *gid, *bad;
+        DPV_TRY(sc.get(&rh, NPD));
+        DPV_TRY(sc.get(&rh_s, NPD));
+        DPV_TRY(sc.get(&ridx, NPD));
+        DPV_TRY(P->alloc(&P->g_rows, NPD));
+        DPV_TRY(sc.get(&flag, NPD));
+        DPV_TRY(sc.get(&gid, NPD));
+        DPV_TRY(sc.get(&bad, 1));
+        k_row_hash<<<grid_for(NPD, B), B, 0, st>>>(NPD, P->rinc_ptr, P->rinc, P->inc_var, rh, ridx);
+        DPV_CHECK_LAUNCH();
+        DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, rh, rh_s, ridx, P->g_rows, (int)NPD, 0, 64,
+                                                   st);
+        }));
+        k_group_flags<<<grid_for(NPD, B), B, 0, st>>>(NPD, rh_s, flag);
+        DPV_CHECK_LAUNCH();
+        DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+            return cub::DeviceScan::InclusiveSum(t, b, flag, gid, (int)NPD, st);
+        }));
+        int32_t ng = 0;
+        DPV_CUDA(cudaMemcpyAsync(&ng, gid + NPD - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        DPV_CUDA(cudaStreamSynchronize(st));
+        // gid is 1-based after the inclusive scan
+        k_sub_one<<<grid_for(NPD, B), B, 0, st>>>(NPD, gid);
+        DPV_CHECK_LAUNCH();
+        int32_t* gstart;
+        DPV_TRY(sc.get(&gstart, ng + 1));
+        DPV_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+        k_group_verify<<<grid_for(NPD, B), B, 0, st>>>(NPD, flag, gid, P->g_rows, P->rinc_ptr,
+                                                        P->rinc, P->inc_var, gstart, bad);
+        DPV_CHECK_LAUNCH();
+        k_group_verify2<<<grid_for(NPD, B), B, 0, st>>>(NPD, gid, gstart, P->g_rows, P->rinc_ptr,
+                                                         P->rinc, P->inc_var, bad);
+        DPV_CHECK_LAUNCH();
+        // host: group sizes and var counts -> chunks
+        std::vector<int32_t> h_gstart(ng), h_rows_head(ng), h_rp;
+        DPV_CUDA(cudaMemcpyAsync(h_gstart.data(), gstart, sizeof(int32_t) * ng,
+                                 cudaMemcpyDeviceToHost, st));
+        int32_t h_bad = 0;
+        DPV_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        std::vector<int32_t> h_rows(NPD), h_rinc_ptr(NPD + 1);
+        DPV_CUDA(cudaMemcpyAsync(h_rows.data(), P->g_rows, sizeof(int32_t) * NPD,
+                                 cudaMemcpyDeviceToHost, st));
+        DPV_CUDA(cudaMemcpyAsync(h_rinc_ptr.data(), P->rinc_ptr, sizeof(int32_t) * (NPD + 1),
+                                 cudaMemcpyDeviceToHost, st));
+        DPV_CUDA(cudaStreamSynchronize(st));
+        if (!h_bad) {
+            std::vector<int4> chunks;
+            int64_t nblk = 0;
+            for (int32_t g = 0; g < ng; ++g) {
+                const int32_t b0 = h_gstart[g], b1 = g + 1 < ng ? h_gstart[g + 1] : (int32_t)NPD;
+                const int32_t head = h_rows[b0];
+                const int m = h_rinc_ptr[head + 1] - h_rinc_ptr[head];
+                if (m == 0) continue;
+                // staged W: 8m rows x (rows + <=16 padding) doubles <= kSyrkSmemDoubles
+                const int rpc = std::min(kSyrkMaxRows,
+                                         ((int)(kSyrkSmemDoubles / (6 * m + 8)) - 16) & ~3);
+                if (rpc < 4) { h_bad = 1; break; }
+                for (int32_t r0 = b0; r0 < b1; r0 += rpc) {
+                    chunks.push_back(make_int4(r0, std::min(rpc, b1 - r0), m, (int)nblk));
+                    nblk += (int64_t)m * (m + 1) / 2;
+                }
+            }
+            if (!h_bad && !chunks.empty() && nblk < (int64_t)1 << 30) {
+                P->n_chunks = (int64_t)chunks.size();
+                P->n_gblocks = nblk;
+                DPV_TRY(P->alloc(&P->g_chunks, P->n_chunks));
+                DPV_CUDA(cudaMemcpyAsync(P->g_chunks, chunks.data(), sizeof(int4) * chunks.size(),
+                                         cudaMemcpyHostToDevice, st));
+                uint64_t *ckey, *ckey_s;
+                int32_t* cblk;
+                DPV_TRY(sc.get(&ckey, nblk));
+                DPV_TRY(sc.get(&ckey_s, nblk));
+                DPV_TRY(sc.get(&cblk, nblk));
+                DPV_TRY(P->alloc(&P->key_blk, nblk));
+                k_chunk_contrib<<<(int)std::min<int64_t>(P->n_chunks, 65535), 128, 0, st>>>(
+                    P->n_chunks, P->g_chunks, P->g_rows, P->rinc_ptr, P->rinc, P->inc_var,
+                    reinterpret_cast<const uint64_t*>(P->union_keys), W, P->n, ckey, cblk);
+                DPV_CHECK_LAUNCH();
+                DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+                    return cub::DeviceRadixSort::SortPairs(t, b, ckey, ckey_s, cblk, P->key_blk,
+                                                           (int)nblk, 0, bits_for(W + 1), st);
+                }));
+                DPV_TRY(P->alloc(&P->key_blk_ptr, W + 1));
+                k_lower_bounds<uint64_t><<<grid_for(W + 1, B), B, 0, st>>>(W, ckey_s, nblk,
+                                                                             P->key_blk_ptr);
+                DPV_CHECK_LAUNCH();
+                DPV_TRY(P->alloc(&P->g_sbuf, nblk * 36));
+                P->grouped = 1;
+            }
+        }
     }
 
     // 11. key -> segment CSR (pose blocks) and var -> segment CSR (rhs_pose)

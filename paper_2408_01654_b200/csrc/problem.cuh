@@ -107,6 +107,15 @@ struct dpv_problem {
     int32_t* run_l = nullptr;      // (NR) first left incidence of the run
     int32_t* run_r = nullptr;      // (NR) first right incidence
     int32_t* run_len = nullptr;    // (NR) pairs in the run
+    // grouped Schur: rows with identical incidence-var lists, SYRK per chunk
+    int32_t grouped = 0;
+    int32_t* g_rows = nullptr;     // (P) rows sorted by group
+    int4* g_chunks = nullptr;      // (n_chunks) {first sorted row, rows, vars m, block offset}
+    int64_t n_chunks = 0;
+    int64_t n_gblocks = 0;
+    double* g_sbuf = nullptr;      // (n_gblocks, 36) chunk Schur blocks
+    int32_t* key_blk_ptr = nullptr;   // (W+1)
+    int32_t* key_blk = nullptr;    // (n_gblocks) chunk blocks of each key, chunk order
     int32_t* key_seg_ptr = nullptr;   // (W+1)
     int32_t* key_seg = nullptr;    // (KS) seg*2 + (negative)
     int32_t* var_seg_ptr = nullptr;   // (n+1)
@@ -185,6 +194,8 @@ struct dpv_problem {
 
 namespace dpv {
 constexpr int kSegMax = 128;      // edges per segment chunk
+constexpr int kSyrkMaxRows = 128;            // rows per grouped-Schur chunk
+constexpr int kSyrkSmemDoubles = 12800;      // 100 KB of W_g staging per chunk (2 CTAs/SM)
 int32_t configure_pool();
 constexpr int kObjBlocks = 1184;  // 148 SMs x 8
 int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int64_t* eidx,

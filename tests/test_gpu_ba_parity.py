@@ -181,3 +181,16 @@ def test_block_cholesky(golden):
                                       np.stack([np.eye(6), -np.eye(6)]), 2)
     with pytest.raises(SingularSystem):
         block_cholesky.block_cholesky(np.array([[0, 0]]), np.eye(6)[None], 2)
+
+
+@pytest.mark.parametrize("case", [c for c in BA_CASES if c[0] in ("loops", "window")])
+def test_grouped_schur_matches_golden(golden, case, monkeypatch):
+    """The opt-in grouped Schur path (per-group SYRK W W^T on DMMA,
+    DPV_SCHUR_GROUPED=1) gives the reference's Schur blocks and rhs_schur."""
+    monkeypatch.setenv("DPV_SCHUR_GROUPED", "1")
+    name, gp, pp = case
+    z = golden(name)
+    g, prob = make(z, gp, pp)
+    sys_ = ba.assemble(prob)
+    close(sys_.schur_blocks, z[pp + "sys_schur_blocks"], 1e-9, 1e-9)
+    close(sys_.rhs_schur, z[pp + "sys_rhs_schur"], 1e-9, 1e-9)

@@ -85,7 +85,7 @@ int main() {
     cudaMalloc(&dc, 16);
     cudaMemcpy(dA, A.data(), 8 * 4096, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    k_bench<<<1, kThreads, kSmemBytes>>>(dA, dL, dX, dc, 20);
+    k_bench<<<1, kThreads, kSmemBytes>>>(dA, dL, dX, dc, getenv("REPS") ? atoi(getenv("REPS")) : 20);
     std::vector<double> L(4096), X(4096);
     long long c[2];
     cudaMemcpy(L.data(), dL, 8 * 4096, cudaMemcpyDeviceToHost);
