@@ -256,6 +256,16 @@ int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1,
                  int32_t h1, int32_t w1, int32_t n_levels, int32_t radius,
                  int32_t dtype, float* out, void* stream);
 
+/* Same, with the sizes of gmap (n_patches) and the fmaps (n_frames): bf16
+ * features with r = 3 and C in {64, 128, 256} take the TMA + tensor-core
+ * kernel (corr_tma.cu; 10x10 tap windows, hardware zero fill outside the
+ * image), everything else the corr.cu kernels. */
+int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                    int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                    int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
+                    int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
+                    void* stream);
+
 /* Level-1 pyramid: 4x4 average pool of channels-last fmap (F,H,W,C) -> (F,H/4,W/4,C). */
 int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
                       int32_t dtype, void* out, void* stream);

@@ -91,6 +91,9 @@ SIGNATURES = {
     "dpv_block_fill_count": (C.c_int32, [vp, C.c_int64, C.c_int64, c_int64_p]),
     "dpv_corr": (C.c_int32, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                              C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp]),
+    "dpv_corr_ex": (C.c_int32, [vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, C.c_int64,
+                                C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int32, C.c_int32, vp, vp]),
 }
 
 _lib = None

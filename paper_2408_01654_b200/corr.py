@@ -45,8 +45,9 @@ def corr(gmap: torch.Tensor, fmaps, coords: torch.Tensor, ii: torch.Tensor, jj: 
         out = torch.empty((E, levels, 9, O, O), dtype=torch.float32, device="cuda")
     f0 = fmaps[0].contiguous()
     f1 = fmaps[1].contiguous() if levels == 2 else None
-    _lib.check(_lib.lib().dpv_corr(
-        _lib.ptr(gmap.contiguous()), _lib.ptr(f0), _lib.ptr(f1),
+    g = gmap.contiguous()
+    _lib.check(_lib.lib().dpv_corr_ex(
+        _lib.ptr(g), int(g.shape[0]), _lib.ptr(f0), _lib.ptr(f1), int(f0.shape[0]),
         _lib.ptr(coords.to(torch.float64).contiguous()), _lib.ptr(ii.to(torch.int32).contiguous()),
         _lib.ptr(jj.to(torch.int32).contiguous()), E, C, f0.shape[1], f0.shape[2],
         f1.shape[1] if f1 is not None else 0, f1.shape[2] if f1 is not None else 0, levels,

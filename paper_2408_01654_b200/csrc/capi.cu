@@ -783,6 +783,37 @@ int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1, const d
                 radius, dtype, out, as_stream(stream));
 }
 
+int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                    int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                    int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
+                    int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
+                    void* stream) {
+    clear_error();
+    DPV_ARG(n_edges >= 0 && channels > 0 && (n_levels == 1 || n_levels == 2) && radius >= 0 &&
+                radius <= 4 && (dtype == 0 || dtype == 1) && n_patches >= 0 && n_frames >= 0,
+            "bad corr args");
+    DPV_ARG(n_edges == 0 || (gmap && fmap0 && coords && ii && jj && out), "NULL corr argument");
+    DPV_ARG(n_levels == 1 || fmap1, "level-1 feature map missing");
+    cudaStream_t st = as_stream(stream);
+    if (n_edges == 0) return DPV_OK;
+    // TMA + tensor-core path: bf16, radius 3, C in {64, 128, 256}
+    if (dtype == 1 && radius == 3 && !getenv("DPV_CORR_NO_TMA")) {
+        bool ok = true;
+        for (int l = 0; l < n_levels && ok; ++l) {
+            const int32_t r = corr_tma(gmap, n_patches, l == 0 ? fmap0 : fmap1, n_frames, coords,
+                                       ii, jj, n_edges, channels, l == 0 ? h0 : h1,
+                                       l == 0 ? w0 : w1, l, n_levels, out, st);
+            if (r == DPV_CUDA_ERROR) return r;
+            ok = r == DPV_OK;
+            if (!ok && l > 0) return r;     // level 0 already written: no mixed paths
+        }
+        if (ok) return DPV_OK;
+        clear_error();
+    }
+    return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,
+                radius, dtype, out, st);
+}
+
 int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
                       int32_t dtype, void* out, void* stream) {
     clear_error();

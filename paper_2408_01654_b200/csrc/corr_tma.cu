@@ -1,0 +1,389 @@
+// K1 on TMA + tensor cores (bf16 features, radius 3), the B200 path of the
+// correlation lookup (Eq. 4; conventions pinned by
+// oracle/corr_oracle.py, see corr.cu).
+//
+// Per (edge, level) item the union of the 9 cells' 8x8 tap grids is a 10x10
+// window of the target frame's feature map (cells of a 3x3 patch lie within
+// ~1 px of each other at 1/4 resolution; wider spreads take a slow path).
+// A PRODUCER warp runs S stages ahead: it reads the item's K2 coordinates,
+// computes the window origin and per-cell offsets / bilinear weights, and
+// issues TMA tile loads (cp.async.bulk.tensor, 128B swizzle, hardware zero
+// fill outside the image) of the window (10x10 taps x 64 channels per box)
+// and of the patch features, completing on an mbarrier.  Four CONSUMER warps
+// run S (16 x 104) = G (16 x C) * Win^T on mma.sync.m16n8k16 (bf16 -> fp32)
+// from the swizzled tiles and blend each cell's 7x7 outputs bilinearly from
+// its 8x8 block of S, then release the stage.  No per-thread address math or
+// bounds checks on the staging path; the dense volume is never stored.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "problem.cuh"
+
+namespace dpv {
+namespace {
+
+constexpr int kCellsT = 9;
+constexpr int kWin = 10;                  // window side (taps)
+constexpr int kTapsPad = 104;             // 13 n-tiles of 8
+constexpr int kHalfBytes = kTapsPad * 128;   // one 64-channel half of the window (swizzled rows)
+constexpr int kGHalfBytes = 16 * 128;     // 16 feature rows x 64 channels
+constexpr int kStages = 3;
+constexpr int kConsumers = 128;
+constexpr int kProducerWarp = 4;
+
+struct CellMeta {
+    int ox, oy;        // cell tap-grid origin inside the window (x0 - r - bx0, y0 - r - by0)
+    float fx, fy;      // bilinear fractions
+};
+struct ItemMeta {
+    CellMeta cell[kCellsT];
+    int bx0, by0, staged, jj;
+    int64_t e;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+                 "r"(tx)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                       int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bar_consumers() {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory");
+}
+
+// 128B swizzle: 16-byte chunk index XOR (row % 8) inside each 1024-byte atom
+__device__ __forceinline__ uint32_t ld_sw(const unsigned char* base, int row, int ch) {
+    return *reinterpret_cast<const uint32_t*>(base + row * 128 + ((((ch >> 3) ^ row) & 7) << 4) +
+                                              (ch & 7) * 2);
+}
+
+__device__ __forceinline__ void mma_bf16_t(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void split(double v, int& i0, float& fr) {
+    if (!(fabs(v) < 1e7)) {
+        i0 = -(1 << 28);
+        fr = 0.f;
+        return;
+    }
+    const double f = floor(v);
+    i0 = (int)f;
+    fr = (float)(v - f);
+}
+
+template <int NH>
+constexpr int stage_bytes() {
+    return ((NH * (kHalfBytes + kGHalfBytes) + (int)sizeof(ItemMeta) + 1023) / 1024) * 1024;
+}
+
+template <int NH>
+__global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
+    const __grid_constant__ CUtensorMap fmap_map, const __grid_constant__ CUtensorMap gmap_map,
+    const __nv_bfloat16* __restrict__ fmap, const __nv_bfloat16* __restrict__ gmap,
+    const double* __restrict__ coords, const int32_t* __restrict__ ii,
+    const int32_t* __restrict__ jj, int64_t E, int H, int Wd, int level, int levels,
+    float* __restrict__ out) {
+    constexpr int C = 64 * NH;
+    constexpr int SB = stage_bytes<NH>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // aligned to 1024 below
+    // 1024-byte aligned stage ring
+    // (pointer arithmetic on the shared array keeps the shared address space)
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    float* S = reinterpret_cast<float*>(sm + kStages * SB);          // 9 x kTapsPad
+    __shared__ uint64_t full[kStages], empty[kStages];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // grid-stride items: the CTAs work on neighbouring edges at any time, so
+    // the target frames' feature maps stay L2-resident (edges grouped by frame)
+    const int64_t n_my = E > blockIdx.x ? (E - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const double scale = level == 0 ? 1.0 : 0.25;
+    constexpr int radius = 3, D = 8, O = 7;
+
+    if (warp == kProducerWarp) {
+        // ---------------- producer ----------------
+        // the next item's coordinates and indices are loaded one item ahead,
+        // so their latency overlaps the current item's hand-off
+        double cxn = 0.0, cyn = 0.0;
+        int32_t iin = 0, jjn = 0;
+        auto fetch = [&](int64_t u) {
+            if (u >= n_my) return;
+            const int64_t e = blockIdx.x + u * (int64_t)gridDim.x;
+            if (lane < kCellsT) {
+                cxn = __ldg(coords + (e * kCellsT + lane) * 2);
+                cyn = __ldg(coords + (e * kCellsT + lane) * 2 + 1);
+            }
+            if (lane == 0) {
+                iin = __ldg(ii + e);
+                jjn = __ldg(jj + e);
+            }
+        };
+        fetch(0);
+        for (int64_t u = 0; u < n_my; ++u) {
+            const int64_t e = blockIdx.x + u * (int64_t)gridDim.x;
+            const int s = (int)(u % kStages);
+            const double cx = cxn, cy = cyn;
+            const int32_t iic = iin, jjc = jjn;
+            fetch(u + 1);
+            mbar_wait(&empty[s], (unsigned)(((u / kStages) & 1) ^ 1));
+            ItemMeta* M = reinterpret_cast<ItemMeta*>(sm + s * SB + NH * (kHalfBytes + kGHalfBytes));
+            int x0 = 0, y0 = 0;
+            float fx = 0.f, fy = 0.f;
+            if (lane < kCellsT) {
+                split(cx * scale, x0, fx);
+                split(cy * scale, y0, fy);
+            }
+            int mnx = lane < kCellsT ? x0 : INT32_MAX, mxx = lane < kCellsT ? x0 : INT32_MIN;
+            int mny = lane < kCellsT ? y0 : INT32_MAX, mxy = lane < kCellsT ? y0 : INT32_MIN;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+                mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+                mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+                mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+            }
+            const int bx0 = mnx - radius, by0 = mny - radius;
+            const bool staged = (mxx - mnx) <= kWin - D && (mxy - mny) <= kWin - D &&
+                                mnx > -(1 << 27);
+            if (lane < kCellsT) {
+                M->cell[lane].ox = x0 - radius - bx0;
+                M->cell[lane].oy = y0 - radius - by0;
+                M->cell[lane].fx = fx;
+                M->cell[lane].fy = fy;
+                // per-cell origin for the slow path
+                if (!staged) {
+                    M->cell[lane].ox = x0 - radius;
+                    M->cell[lane].oy = y0 - radius;
+                }
+            }
+            if (lane == 0) {
+                M->bx0 = bx0;
+                M->by0 = by0;
+                M->staged = staged ? 1 : 0;
+                M->jj = jjc;
+                M->e = e;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                unsigned char* st = sm + s * SB;
+                const unsigned tx = NH * kGHalfBytes + (staged ? NH * kWin * kWin * 128 : 0);
+                mbar_arrive_tx(&full[s], tx);
+                const int grow = iic * kCellsT;
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    tma_2d(st + NH * kHalfBytes + h * kGHalfBytes, &gmap_map, 64 * h, grow,
+                           &full[s]);
+                    if (staged)
+                        tma_4d(st + h * kHalfBytes, &fmap_map, 64 * h, bx0, by0, M->jj, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers (4 warps) ----------------
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int64_t u = 0; u < n_my; ++u) {
+        const int s = (int)(u % kStages);
+        mbar_wait(&full[s], (unsigned)((u / kStages) & 1));
+        const unsigned char* st = sm + s * SB;
+        const ItemMeta* M = reinterpret_cast<const ItemMeta*>(st + NH * (kHalfBytes + kGHalfBytes));
+        const unsigned char* Gs = st + NH * kHalfBytes;
+        float* o = out + ((M->e * levels + level) * kCellsT) * (int64_t)(O * O);
+        if (M->staged) {
+            float acc[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const unsigned char* Wh = st + h * kHalfBytes;
+                const unsigned char* Gh = Gs + h * kGHalfBytes;
+#pragma unroll
+                for (int k0 = 0; k0 < 64; k0 += 16) {
+                    uint32_t a[4];
+                    a[0] = ld_sw(Gh, g, k0 + 2 * t4);
+                    a[1] = ld_sw(Gh, g + 8, k0 + 2 * t4);
+                    a[2] = ld_sw(Gh, g, k0 + 2 * t4 + 8);
+                    a[3] = ld_sw(Gh, g + 8, k0 + 2 * t4 + 8);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int nt = warp + 4 * q;
+                        if (nt < 13) {
+                            const int n = nt * 8 + g;
+                            mma_bf16_t(acc[q], a, ld_sw(Wh, n, k0 + 2 * t4),
+                                       ld_sw(Wh, n, k0 + 2 * t4 + 8));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int nt = warp + 4 * q;
+                if (nt < 13) {
+                    const int col = nt * 8 + 2 * t4;
+                    S[g * kTapsPad + col] = acc[q][0];
+                    S[g * kTapsPad + col + 1] = acc[q][1];
+                    if (g == 0) {
+                        S[8 * kTapsPad + col] = acc[q][2];
+                        S[8 * kTapsPad + col + 1] = acc[q][3];
+                    }
+                }
+            }
+            bar_consumers();
+            for (int x = tid; x < kCellsT * O * O; x += kConsumers) {
+                const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
+                const CellMeta cm = M->cell[c];
+                const float* sp = S + c * kTapsPad + (cm.oy + a) * kWin + cm.ox + bb;
+                o[x] = (1.f - cm.fy) * ((1.f - cm.fx) * sp[0] + cm.fx * sp[1]) +
+                       cm.fy * ((1.f - cm.fx) * sp[kWin] + cm.fx * sp[kWin + 1]);
+            }
+        } else {
+            // wide or non-finite window: per-cell integer-tap dots from global memory
+            const __nv_bfloat16* fp = fmap + (int64_t)M->jj * H * Wd * C;
+            const __nv_bfloat16* gp = gmap + (int64_t)ii[M->e] * kCellsT * C;
+            for (int x = tid; x < kCellsT * D * D; x += kConsumers) {
+                const int c = x / (D * D), ty = (x % (D * D)) / D, tx = x % D;
+                const int py = M->cell[c].oy + ty, px = M->cell[c].ox + tx;
+                float acc = 0.f;
+                if (py >= 0 && py < H && px >= 0 && px < Wd) {
+                    const __nv_bfloat16* f = fp + ((int64_t)py * Wd + px) * C;
+                    for (int k = 0; k < C; ++k)
+                        acc += __bfloat162float(f[k]) * __bfloat162float(gp[c * C + k]);
+                }
+                S[c * kTapsPad + ty * D + tx] = acc;
+            }
+            bar_consumers();
+            for (int x = tid; x < kCellsT * O * O; x += kConsumers) {
+                const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
+                const float dx = M->cell[c].fx, dy = M->cell[c].fy;
+                const float* sp = S + c * kTapsPad + a * D + bb;
+                o[x] = (1.f - dy) * ((1.f - dx) * sp[0] + dx * sp[1]) +
+                       dy * ((1.f - dx) * sp[D] + dx * sp[D + 1]);
+            }
+        }
+        bar_consumers();          // S and the stage are free
+        mbar_arrive(&empty[s]);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+// bf16 features, radius 3, C in {64, 128, 256}; returns DPV_BAD_ARGS when the
+// TMA path does not apply (the caller falls back to corr.cu)
+int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap, int64_t n_frames,
+                 const double* coords, const int32_t* ii, const int32_t* jj, int64_t E, int C,
+                 int H, int Wd, int level, int levels, float* out, cudaStream_t st) {
+    auto enc = encode_fn();
+    if (!enc || (C != 64 && C != 128 && C != 256) || n_patches < 1 || n_frames < 1 ||
+        (reinterpret_cast<uintptr_t>(fmap) & 15) || (reinterpret_cast<uintptr_t>(gmap) & 15))
+        return DPV_BAD_ARGS;
+    CUtensorMap fm, gm;
+    {
+        const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)Wd, (cuuint64_t)H,
+                                    (cuuint64_t)n_frames};
+        const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)Wd * C * 2,
+                                       (cuuint64_t)H * Wd * C * 2};
+        const cuuint32_t box[4] = {64, kWin, kWin, 1};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        if (enc(&fm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(fmap), dims, strides,
+                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return DPV_BAD_ARGS;
+    }
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)n_patches * kCellsT};
+        const cuuint64_t strides[1] = {(cuuint64_t)C * 2};
+        const cuuint32_t box[2] = {64, 16};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&gm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(gmap), dims, strides,
+                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return DPV_BAD_ARGS;
+    }
+    auto launch = [&](auto kern, int sb) -> int32_t {
+        const size_t smem = (size_t)kStages * sb + sizeof(float) * kCellsT * kTapsPad + 1024;
+        static size_t cur[3] = {0, 0, 0};
+        const int slot = C == 64 ? 0 : (C == 128 ? 1 : 2);
+        DPV_TRY(ensure_smem(kern, smem, cur[slot]));
+        int per_sm = 0;
+        DPV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kConsumers + 32,
+                                                               smem));
+        const int64_t want = (int64_t)sm_count() * std::max(1, per_sm);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(E, want));
+        DPV_TSTART("corr", st);
+        kern<<<grid, kConsumers + 32, smem, st>>>(fm, gm, reinterpret_cast<const __nv_bfloat16*>(fmap),
+                                                  reinterpret_cast<const __nv_bfloat16*>(gmap),
+                                                  coords, ii, jj, E, H, Wd, level, levels, out);
+        DPV_CHECK_LAUNCH();
+        return DPV_OK;
+    };
+    if (C == 64) return launch(k_corr_tma<1>, stage_bytes<1>());
+    if (C == 128) return launch(k_corr_tma<2>, stage_bytes<2>());
+    return launch(k_corr_tma<4>, stage_bytes<4>());
+}
+
+}  // namespace dpv

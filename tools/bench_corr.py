@@ -39,11 +39,13 @@ def main():
         jj, _ = torch.sort(jj)
     out = torch.empty((E, 2, 9, 7, 7), dtype=torch.float32, device="cuda")
     hbm_bytes = E * (144 + 8 + 2 * 441 * 4) + E * 9 * C * 2 + sum(p.numel() * 2 for p in pyr)
-    for mode in ("mma", "fma"):
+    for mode in ("tma", "mma", "fma"):
+        os.environ.pop("DPV_CORR_FMA", None)
+        os.environ.pop("DPV_CORR_NO_TMA", None)
+        if mode != "tma":
+            os.environ["DPV_CORR_NO_TMA"] = "1"
         if mode == "fma":
             os.environ["DPV_CORR_FMA"] = "1"
-        else:
-            os.environ.pop("DPV_CORR_FMA", None)
         for _ in range(3):
             corr.corr(gmap, pyr, coords, ii, jj, out=out)
         torch.cuda.synchronize()
