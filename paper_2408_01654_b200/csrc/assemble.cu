@@ -820,10 +820,10 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
         p->e_terms, p->seg_h, p->seg_g)
         switch (variant) {
-            case 1: DPV_ASM(1, 4); break;
+            case 1: DPV_ASM(9, 2); break;
             case 2: DPV_ASM(1, 3); break;
             case 3: DPV_ASM(2, 3); break;
-            case 4: DPV_ASM(1, 2); break;
+            case 4: DPV_ASM(9, 1); break;
             case 5: DPV_ASM(3, 2); break;
             default: DPV_ASM(3, 3); break;
         }
