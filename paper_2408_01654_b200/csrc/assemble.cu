@@ -126,9 +126,13 @@ __global__ void __launch_bounds__(256) k_objective(
     }
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
+}
+
 // same sum, one warp per (src, dst) segment: the two frames are loaded once
 // per segment into shared memory, lanes stride over the segment's edges.
-template <int M, int U, int MINB>
+template <int M, int U, int MINB, bool PF>
 __global__ void __launch_bounds__(256, MINB) k_objective_seg(
     int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
     const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
@@ -156,7 +160,24 @@ __global__ void __launch_bounds__(256, MINB) k_objective_seg(
             fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
         }
         __syncwarp();
+        int32_t rn1 = (PF && e0 + lane + 32 < e1) ? a_row[e0 + lane + 32] : 0;
         for (int32_t e = e0 + lane; e < e1; e += 32) {
+            if (PF) {          // next edge's inputs into L1 (see k_assemble_edges)
+                const int32_t en = e + 32;
+                int32_t rn2 = 0;
+                if (en < e1) {
+#pragma unroll
+                    for (int c = 0; c < 2 * M; ++c) {
+                        prefetch_l1(a_tgt + (int64_t)c * E + en);
+                        prefetch_l1(r_ray + (int64_t)c * P + rn1);
+                    }
+                    prefetch_l1(a_w + en);
+                    prefetch_l1(a_w + E + en);
+                    prefetch_l1(d + rn1);
+                    if (en + 32 < e1) rn2 = a_row[en + 32];
+                }
+                rn1 = rn2;
+            }
             const int32_t row = a_row[e];
             const double id = __drcp_rn(__ldg(d + row));
             const double w0 = a_w[e], w1 = a_w[E + e];
@@ -299,7 +320,7 @@ __device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
     return a * 6 - (a * (a - 1)) / 2 + (b - a);
 }
 
-template <int M, int U, int MINB>
+template <int M, int U, int MINB, bool PF>
 __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
     int64_t S, int64_t E, int m_unused, int64_t P, const int32_t* __restrict__ seg_ptr,
     const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
@@ -331,7 +352,27 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
         for (int k = 0; k < 21; ++k) H[k] = 0.0;
 #pragma unroll
         for (int k = 0; k < 6; ++k) G[k] = 0.0;
+        // software prefetch (PF): the lane's next edge (e + 32) gets its targets,
+        // weights, rays and depth pulled into L1 one edge ahead; its row index
+        // is loaded two edges ahead
+        int32_t rn1 = (PF && e0 + lane + 32 < e1) ? a_row[e0 + lane + 32] : 0;
         for (int32_t e = e0 + lane; e < e1; e += 32) {
+            if (PF) {
+                const int32_t en = e + 32;
+                int32_t rn2 = 0;
+                if (en < e1) {
+#pragma unroll
+                    for (int c = 0; c < 2 * M; ++c) {
+                        prefetch_l1(a_tgt + (int64_t)c * E + en);
+                        prefetch_l1(r_ray + (int64_t)c * P + rn1);
+                    }
+                    prefetch_l1(a_w + en);
+                    prefetch_l1(a_w + E + en);
+                    prefetch_l1(d + rn1);
+                    if (en + 32 < e1) rn2 = a_row[en + 32];
+                }
+                rn1 = rn2;
+            }
             const int32_t row = a_row[e];
             const double dd = __ldg(d + row);
             const double id = __drcp_rn(dd);
@@ -724,20 +765,15 @@ int32_t objective(dpv_problem* p, const double* q, const double* t, const double
     if (p->m == 9 && p->S > 0)
     {
         const int variant = getenv("DPV_OBJ_VARIANT") ? atoi(getenv("DPV_OBJ_VARIANT")) : 0;
-#define DPV_OBJ(U, B)                                                                        \
-    k_objective_seg<9, U, B><<<kObjBlocks, 256, 0, st>>>(                                    \
+#define DPV_OBJ(U, B, PF)                                                                    \
+    k_objective_seg<9, U, B, PF><<<kObjBlocks, 256, 0, st>>>(                                \
         p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,    \
         p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3], p->obj_part)
         switch (variant) {
-            case 1: DPV_OBJ(1, 4); break;
-            case 2: DPV_OBJ(3, 3); break;
-            case 3: DPV_OBJ(9, 3); break;
-            case 4: DPV_OBJ(1, 3); break;
-            case 5: DPV_OBJ(2, 4); break;
-            case 6: DPV_OBJ(3, 4); break;
-            case 7: DPV_OBJ(1, 5); break;
-            case 8: DPV_OBJ(9, 2); break;
-            default: DPV_OBJ(3, 4); break;
+            case 1: DPV_OBJ(3, 4, false); break;
+            case 2: DPV_OBJ(1, 4, true); break;
+            case 3: DPV_OBJ(3, 3, true); break;
+            default: DPV_OBJ(3, 4, true); break;
         }
 #undef DPV_OBJ
     }
@@ -814,18 +850,16 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
                                             (int64_t)sm_count() * 64);
         DPV_TSTART("assemble_edges", st);
         const int variant = getenv("DPV_ASM_VARIANT") ? atoi(getenv("DPV_ASM_VARIANT")) : 0;
-#define DPV_ASM(U, B)                                                                          \
-    k_assemble_edges<9, U, B><<<blocks, 32 * warps_per_block, 0, st>>>(                        \
+#define DPV_ASM(U, B, PF)                                                                      \
+    k_assemble_edges<9, U, B, PF><<<blocks, 32 * warps_per_block, 0, st>>>(                    \
         p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,        \
         p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
         p->e_terms, p->seg_h, p->seg_g)
         switch (variant) {
-            case 1: DPV_ASM(9, 2); break;
-            case 2: DPV_ASM(1, 3); break;
-            case 3: DPV_ASM(2, 3); break;
-            case 4: DPV_ASM(9, 1); break;
-            case 5: DPV_ASM(3, 2); break;
-            default: DPV_ASM(3, 3); break;
+            case 1: DPV_ASM(3, 3, false); break;
+            case 2: DPV_ASM(1, 3, true); break;
+            case 3: DPV_ASM(3, 2, true); break;
+            default: DPV_ASM(3, 3, true); break;
         }
 #undef DPV_ASM
         DPV_CHECK_LAUNCH();
