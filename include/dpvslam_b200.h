@@ -266,6 +266,15 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
                     int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
                     void* stream);
 
+/* Proximity loop-closure candidates (loop.py:64-85): centers (n_frames, 3)
+ * DEVICE f64 camera centres; pairs (capacity, 2) DEVICE int64 (old, recent),
+ * sorted by centre distance (ties: recent, then old ascending) exactly as the
+ * reference; *count (HOST) = number of pairs.  Pass pairs = NULL to query
+ * the count only.  Candidates: recent - old >= min_gap, distance < threshold. */
+int32_t dpv_proximity_detect(const double* centers, int64_t n_frames, int64_t min_gap,
+                             double threshold, int64_t* pairs, int64_t capacity, int64_t* count,
+                             void* stream);
+
 /* Level-1 pyramid: 4x4 average pool of channels-last fmap (F,H,W,C) -> (F,H/4,W/4,C). */
 int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
                       int32_t dtype, void* out, void* stream);

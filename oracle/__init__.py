@@ -10,7 +10,8 @@ Who may import it: ``tests/``, ``__graft_entry__.smoke()`` and the
 ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py``.  The product
 package ``paper_2408_01654_b200`` never imports it and has no CPU fallback.
 
-Pinning: ``ba_oracle`` / ``geometry_oracle`` / ``cholesky_oracle`` are checked
+Pinning: ``ba_oracle`` / ``geometry_oracle`` / ``cholesky_oracle`` /
+``loop_oracle`` are checked
 against golden fixtures produced by the real reference
 (``tests/golden/make_golden.py``; ``tests/test_oracle_golden.py``).
 ``corr_oracle`` has no reference implementation (SPEC.md:14 puts Eq. 4 out of

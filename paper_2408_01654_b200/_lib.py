@@ -87,6 +87,8 @@ SIGNATURES = {
     "dpv_cholesky_solve": (C.c_int32, [vp, vp, C.c_int64, vp, vp]),
     "dpv_block_sparse_solve": (C.c_int32, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
     "dpv_problem_spd_info": (C.c_int32, [vp, c_int64_p]),
+    "dpv_proximity_detect": (C.c_int32, [vp, C.c_int64, C.c_int64, C.c_double, vp, C.c_int64,
+                                         c_int64_p, vp]),
     "dpv_reproject_coords_sel": (C.c_int32, [vp, vp, vp, vp, C.c_double, vp, C.c_int64, vp, vp]),
     "dpv_block_fill_count": (C.c_int32, [vp, C.c_int64, C.c_int64, c_int64_p]),
     "dpv_corr": (C.c_int32, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,

@@ -814,6 +814,16 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
                 radius, dtype, out, st);
 }
 
+int32_t dpv_proximity_detect(const double* centers, int64_t n_frames, int64_t min_gap,
+                             double threshold, int64_t* pairs, int64_t capacity, int64_t* count,
+                             void* stream) {
+    clear_error();
+    DPV_ARG(count && (n_frames == 0 || centers) && min_gap >= 0 && n_frames >= 0,
+            "bad detect args");
+    return proximity_detect(centers, n_frames, min_gap, threshold, pairs, capacity, count,
+                            as_stream(stream));
+}
+
 int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
                       int32_t dtype, void* out, void* stream) {
     clear_error();

@@ -217,6 +217,8 @@ int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap, int64_t 
 int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const double* coords,
              const int32_t* ii, const int32_t* jj, int64_t E, int C, int h0, int w0, int h1,
              int w1, int levels, int radius, int dtype, float* out, cudaStream_t st);
+int32_t proximity_detect(const double* centers, int64_t n, int64_t gap, double thr,
+                         int64_t* pairs, int64_t cap, int64_t* count, cudaStream_t st);
 int32_t coords_sel(dpv_problem* p, const double* q, const double* t, const double* d,
                    double scale, const int64_t* sel, int64_t n_sel, double* out,
                    cudaStream_t st);

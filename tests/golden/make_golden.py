@@ -319,6 +319,33 @@ def case_cholesky():
 # synthetic-generator hashes (inputs of configs 1-3)
 
 
+def case_detect():
+    """Proximity loop-closure candidates (pkg/src/patchslam/loop.py:51-85):
+    camera centres of a few synthetic trajectories that revisit themselves,
+    reference detect() output in its distance order (stable for ties)."""
+    from patchslam.loop import ProximityConfig, detect, resolve_threshold
+    out = {}
+    k = 0
+    for kind, n, gap, thr, newest in [("circle", 120, 30, None, None),
+                                      ("square-loop", 200, 31, None, None),
+                                      ("circle", 90, 40, 0.9, 85),
+                                      ("circle", 60, 40, None, 30),
+                                      ("line", 150, 30, 3.0, None)]:
+        spec = SceneSpec(kind=kind, n_frames=n, seed=k, n_landmarks=4 * n, look="forward",
+                         extent=12.0, overshoot=0.2)
+        scene, graph = generate(spec, patches_per_frame=2, odometry_radius=3)
+        cfg = ProximityConfig(distance_threshold=thr, min_temporal_gap=gap)
+        pairs = detect(graph, cfg, newest=newest)
+        out[f"d{k}_centers"] = graph.camera_centers()
+        out[f"d{k}_gap"] = np.int64(gap)
+        out[f"d{k}_threshold"] = np.float64(resolve_threshold(graph, cfg))
+        out[f"d{k}_newest"] = np.int64(-1 if newest is None else newest)
+        out[f"d{k}_pairs"] = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+        k += 1
+    out["n_cases"] = np.int64(k)
+    save("detect", out)
+
+
 def soa_hashes(graph) -> dict:
     h = {}
     for k, v in graph_soa(graph).items():
@@ -389,6 +416,7 @@ if __name__ == "__main__":
     args = ap.parse_args()
     cases = {"small": case_small, "window": case_window, "loops": case_loops,
              "edges": case_edges, "reproject": case_reproject, "cholesky": case_cholesky,
+             "detect": case_detect,
              "synth": lambda: case_synth(args.with_cfg3)}
     for name, fn in cases.items():
         if args.only and name not in args.only.split(","):

@@ -172,3 +172,16 @@ def test_block_cholesky_singular_cases():
         O.block_cholesky(np.array([[0, 0], [1, 1]]), np.stack([np.eye(6), -np.eye(6)]), 2)
     with pytest.raises(O.OracleSingular):
         O.block_cholesky(np.array([[0, 0]]), np.eye(6)[None], 2)
+
+
+def test_detect_oracle_matches_reference(golden):
+    """oracle/loop_oracle.py reproduces the reference's proximity candidates
+    (loop.py:64-85) in order, on the reference's own fixtures."""
+    from oracle import loop_oracle
+    z = golden("detect")
+    for k in range(int(z["n_cases"])):
+        c = z[f"d{k}_centers"]
+        newest = int(z[f"d{k}_newest"])
+        pairs = loop_oracle.detect(c, int(z[f"d{k}_gap"]), float(z[f"d{k}_threshold"]),
+                                   None if newest < 0 else newest)
+        assert np.array_equal(np.asarray(pairs, dtype=np.int64).reshape(-1, 2), z[f"d{k}_pairs"])
