@@ -423,6 +423,9 @@ int32_t dpv_problem_array(const dpv_problem* p, const char* name, void** ptr, in
                           int32_t* dtype) {
     clear_error();
     DPV_ARG(p && name && ptr && count && dtype, "NULL argument");
+    const std::string nm(name);
+    if (nm == "pair_l" || nm == "pair_r" || nm == "key_pair_ptr")
+        DPV_TRY(ensure_pairs(const_cast<dpv_problem*>(p)));   // lazily expanded from runs
     ArrayDesc a;
     if (!lookup(p, name, a)) {
         set_error(std::string("unknown array ") + name);

@@ -7,6 +7,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 
@@ -266,73 +267,6 @@ __global__ void k_pair_counts(int64_t P, const int32_t* rinc_ptr, int64_t* npair
     }
 }
 
-// all (l <= r) incidence pairs of each depth row, row-major: the reference's
-// keep = s_var[left] <= s_var[right] with vars ascending and unique per row
-__global__ void k_pairs(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
-                        const int32_t* inc_var, const int64_t* pair_off, int64_t nfree,
-                        uint64_t* key, int32_t* pl, int32_t* pr) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < P; r += nwarps) {
-        const int32_t s = rinc_ptr[r];
-        const int32_t m = rinc_ptr[r + 1] - s;
-        const int64_t base = pair_off[r];
-        const int64_t tot = (int64_t)m * (m + 1) / 2;
-        for (int64_t k = lane; k < tot; k += 32) {
-            // invert k -> (l, rr) for the row-major upper triangle
-            int32_t l = 0;
-            int64_t rowlen = m, acc = 0;
-            while (acc + rowlen <= k) { acc += rowlen; --rowlen; ++l; }
-            int32_t rr = l + (int32_t)(k - acc);
-            int32_t il = rinc[s + l], ir = rinc[s + rr];
-            key[base + k] = (uint64_t)inc_var[il] * (uint64_t)nfree + (uint64_t)inc_var[ir];
-            pl[base + k] = il;
-            pr[base + k] = ir;
-        }
-    }
-}
-
-// Schur pair runs: pair k starts a run unless it continues the previous pair
-// of the same key with both incidences advanced by one
-__global__ void k_run_flags(int64_t n, const uint64_t* key, const int32_t* pl, const int32_t* pr,
-                            int32_t* flag) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        if (k == n) {
-            flag[k] = 0;
-            continue;
-        }
-        flag[k] = (k == 0 || key[k] != key[k - 1] || pl[k] != pl[k - 1] + 1 ||
-                   pr[k] != pr[k - 1] + 1) ? 1 : 0;
-    }
-}
-
-__global__ void k_run_fill(int64_t n, const int32_t* flag, const int32_t* rid, const int32_t* pl,
-                           const int32_t* pr, int32_t* run_l, int32_t* run_r, int64_t* run_start) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        if (!flag[k]) continue;
-        const int32_t r = rid[k];
-        run_l[r] = pl[k];
-        run_r[r] = pr[k];
-        run_start[r] = k;
-    }
-}
-
-__global__ void k_run_len(int64_t nr, int64_t n, const int64_t* run_start, int32_t* run_len) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr;
-         r += (int64_t)gridDim.x * blockDim.x)
-        run_len[r] = (int32_t)((r + 1 < nr ? run_start[r + 1] : n) - run_start[r]);
-}
-
-__global__ void k_key_runs(int64_t W, const int64_t* key_pair_ptr, const int32_t* rid,
-                           int32_t* key_run_ptr) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= W;
-         w += (int64_t)gridDim.x * blockDim.x)
-        key_run_ptr[w] = rid[key_pair_ptr[w]];
-}
-
 // ---- grouped Schur index: rows with identical incidence-var lists ---------
 __global__ void k_row_hash(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
                            const int32_t* inc_var, uint64_t* h, int32_t* idx) {
@@ -413,6 +347,108 @@ __global__ void k_sub_one(int64_t n, int32_t* a) {
         a[i] -= 1;
 }
 
+// Schur pair runs without materialising the pairs.  Pair (il, ir) of a depth
+// row continues a run iff (il-1, ir-1) is a pair of the same key: both
+// incidences belong to the same vars and share a row.  MODE 0 counts the run
+// heads per row, MODE 1 writes them in pair order (deterministic).
+template <int MODE>
+__global__ void k_pair_heads(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
+                             const int32_t* inc_var, const int32_t* inc_row, int64_t nfree,
+                             int32_t* hcount, const int64_t* hoff, uint64_t* hkey, int32_t* hl,
+                             int32_t* hr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < P; r += nwarps) {
+        const int32_t s = rinc_ptr[r];
+        const int32_t m = rinc_ptr[r + 1] - s;
+        const int64_t tot = (int64_t)m * (m + 1) / 2;
+        int64_t base = MODE ? hoff[r] : 0;
+        int32_t cnt = 0;
+        for (int64_t k0 = 0; k0 < tot; k0 += 32) {
+            const int64_t k = k0 + lane;
+            bool head = false;
+            int32_t il = 0, ir = 0;
+            if (k < tot) {
+                int32_t l = 0;
+                int64_t rowlen = m, acc = 0;
+                while (acc + rowlen <= k) { acc += rowlen; --rowlen; ++l; }
+                const int32_t rr = l + (int32_t)(k - acc);
+                il = rinc[s + l];
+                ir = rinc[s + rr];
+                head = !(il > 0 && ir > 0 && inc_var[il - 1] == inc_var[il] &&
+                         inc_var[ir - 1] == inc_var[ir] && inc_row[il - 1] == inc_row[ir - 1]);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, head);
+            if (MODE == 1 && head) {
+                const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
+                hkey[pos] = (uint64_t)inc_var[il] * (uint64_t)nfree + (uint64_t)inc_var[ir];
+                hl[pos] = il;
+                hr[pos] = ir;
+            }
+            cnt += __popc(bal);
+        }
+        if (MODE == 0 && lane == 0) hcount[r] = cnt;
+    }
+}
+
+// run length: warp per head, 32 offsets per probe
+__global__ void k_run_extent(int64_t NR, int64_t I, const int32_t* run_l, const int32_t* run_r,
+                             const int32_t* inc_var, const int32_t* inc_row, int32_t* run_len) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = warp; q < NR; q += nwarps) {
+        const int32_t il = run_l[q], ir = run_r[q];
+        const int32_t a = inc_var[il], b = inc_var[ir];
+        int32_t len = 0;
+        for (int32_t t0 = 0;; t0 += 32) {
+            const int32_t t = t0 + lane;
+            const bool ok = il + t < I && ir + t < I && inc_var[il + t] == a &&
+                            inc_var[ir + t] == b && inc_row[il + t] == inc_row[ir + t];
+            const unsigned bal = __ballot_sync(0xffffffffu, ok);
+            if (bal != 0xffffffffu) {
+                len = t0 + __ffs(~bal) - 1;
+                break;
+            }
+        }
+        if (lane == 0) run_len[q] = len;
+    }
+}
+
+// lazily materialised pairs (parity export): run q -> pairs off[q] + t
+__global__ void k_expand_runs(int64_t NR, const int64_t* off, const int32_t* run_l,
+                              const int32_t* run_r, const int32_t* run_len, int32_t* pl,
+                              int32_t* pr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = warp; q < NR; q += nwarps)
+        for (int32_t t = lane; t < run_len[q]; t += 32) {
+            pl[off[q] + t] = run_l[q] + t;
+            pr[off[q] + t] = run_r[q] + t;
+        }
+}
+
+__global__ void k_key_pair_ptr(int64_t W, const int32_t* key_run_ptr, const int64_t* off,
+                               int64_t* key_pair_ptr) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= W;
+         w += (int64_t)gridDim.x * blockDim.x)
+        key_pair_ptr[w] = off[key_run_ptr[w]];
+}
+
+__global__ void k_i32_to_i64(int64_t n, const int32_t* a, int64_t* b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+__global__ void k_i64_to_i32(int64_t n, const int64_t* a, int32_t* b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (int32_t)a[i];
+}
+
 __global__ void k_gather_i32(int64_t n, const int32_t* idx, const int32_t* src, int32_t* dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -487,6 +523,22 @@ int32_t frame_rotations(dpv_problem* p, const double* q, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------
 
+// DPV_BUILD_PROFILE=1: per-phase wall times of the index build (synchronising)
+struct PhaseTimer {
+    bool on = getenv("DPV_BUILD_PROFILE") != nullptr;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    explicit PhaseTimer(cudaStream_t s) : st(s) {}
+    void lap(const char* name) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[dpv build] %-28s %8.3f ms\n", name,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int64_t* eidx_in,
                       int64_t n_eidx, const int64_t* extra_keys, int64_t n_extra,
                       cudaStream_t st, dpv_problem* P) {
@@ -508,6 +560,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     DPV_TRY(P->alloc(&P->count_buf, 4));
     dcount = P->count_buf;
 
+    PhaseTimer ptimer(st);
     // 1. edge selection (ba.py:72-77)
     if (eidx_in) {
         P->E = n_eidx;
@@ -551,6 +604,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
 
+    ptimer.lap("before 2. depth keys = sort");
     // 2. depth keys = sorted {(src_frame, src_patch)} (ba.py:80-83)
     {
         int32_t* sorted;
@@ -575,6 +629,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
 
+    ptimer.lap("before 3. touched fixed fra");
     // 3. touched fixed frames (ba.py:89-95)
     {
         int32_t* fl;
@@ -603,6 +658,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         }
     }
 
+    ptimer.lap("before 4. segments: stable ");
     // 4. segments: stable sort by (src, dst), chunks of <= kSegMax edges
     int32_t* perm;
     DPV_TRY(sc.get(&perm, E));
@@ -652,6 +708,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CUDA(cudaStreamSynchronize(st));
     }
 
+    ptimer.lap("before 5. assembly-order So");
     // 5. assembly-order SoA copies (ba.py:124-141 structure, permuted)
     DPV_TRY(P->alloc(&P->a_src, E));
     DPV_TRY(P->alloc(&P->a_dst, E));
@@ -679,6 +736,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
 
+    ptimer.lap("before 6. per-row CSR over ");
     // 6. per-row CSR over assembly positions
     DPV_TRY(P->alloc(&P->row_ptr, NPD + 1));
     DPV_TRY(P->alloc(&P->row_pos, E));
@@ -700,6 +758,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
 
+    ptimer.lap("before 7. incidences (ba.py");
     // 7. incidences (ba.py:175-182): unique (var, row) keys of the source- and
     //    target-side rows, with the contribution CSR and inc_inv
     int32_t* inc_inv_tmp = nullptr;
@@ -801,6 +860,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
                                                                   P->var_inc_ptr);
     DPV_CHECK_LAUNCH();
 
+    ptimer.lap("before 8. incidences per de");
     // 8. incidences per depth row, ascending var (ba.py:185-189 `order`)
     DPV_TRY(P->alloc(&P->rinc_ptr, NPD + 1));
     DPV_TRY(P->alloc(&P->rinc, I));
@@ -822,8 +882,11 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
 
-    // 9. Schur pairs per row (ba.py:190-199), then CSR by folded key
-    uint64_t* pkey_sorted = nullptr;
+    ptimer.lap("before 9. Schur pairs per r");
+    // 9. Schur pairs per row (ba.py:190-199) in run-length form: only the run
+    // heads are enumerated and sorted by folded key (stable -> row order); the
+    // pair list itself is materialised lazily for the parity export
+    uint64_t* hkey_s = nullptr;
     {
         int64_t *npair, *poff;
         DPV_TRY(sc.get(&npair, NPD + 1));
@@ -837,41 +900,65 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
             return cub::DeviceScan::ExclusiveSum(t, b, npair, poff, (int)NPD + 1, st);
         }));
         DPV_TRY(read_scalar(poff + NPD, &P->NP, st));
-        const int64_t NPR = P->NP;
-        DPV_ARG(NPR < (int64_t)2000000000, "too many Schur pairs for int32 CUB sorts");
-        uint64_t* pk;
-        int32_t *pl, *pr, *pid, *pid_s;
-        DPV_TRY(sc.get(&pk, NPR));
-        DPV_TRY(sc.get(&pkey_sorted, NPR));
-        DPV_TRY(sc.get(&pl, NPR));
-        DPV_TRY(sc.get(&pr, NPR));
-        DPV_TRY(sc.get(&pid, NPR));
-        DPV_TRY(sc.get(&pid_s, NPR));
+        int32_t* hcount;
+        int64_t *hcount64, *hoff;
+        DPV_TRY(sc.get(&hcount, NPD + 1));
+        DPV_TRY(sc.get(&hcount64, NPD + 1));
+        DPV_TRY(sc.get(&hoff, NPD + 1));
         if (NPD > 0) {
-            k_pairs<<<grid_for(NPD * 32, B), B, 0, st>>>(NPD, P->rinc_ptr, P->rinc, P->inc_var,
-                                                         poff, P->n, pk, pl, pr);
+            k_pair_heads<0><<<grid_for(NPD * 32, B), B, 0, st>>>(
+                NPD, P->rinc_ptr, P->rinc, P->inc_var, P->inc_row, P->n, hcount, nullptr, nullptr,
+                nullptr, nullptr);
+            DPV_CHECK_LAUNCH();
+            k_i32_to_i64<<<grid_for(NPD, B), B, 0, st>>>(NPD, hcount, hcount64);
             DPV_CHECK_LAUNCH();
         }
-        if (NPR > 0) {
-            k_iota<<<grid_for(NPR, B), B, 0, st>>>(NPR, pid);
-            DPV_CHECK_LAUNCH();
-        }
-        int eb = bits_for((uint64_t)P->n * (uint64_t)P->n);
+        DPV_CUDA(cudaMemsetAsync(hcount64 + NPD, 0, sizeof(int64_t), st));
         DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortPairs(t, b, pk, pkey_sorted, pid, pid_s, (int)NPR, 0,
-                                                   eb, st);
+            return cub::DeviceScan::ExclusiveSum(t, b, hcount64, hoff, (int)NPD + 1, st);
         }));
-        DPV_TRY(P->alloc(&P->pair_l, NPR));
-        DPV_TRY(P->alloc(&P->pair_r, NPR));
-        if (NPR > 0) {
-            k_gather_i32<<<grid_for(NPR, B), B, 0, st>>>(NPR, pid_s, pl, P->pair_l);
+        int64_t nr = 0;
+        DPV_TRY(read_scalar(hoff + NPD, &nr, st));
+        P->NR = nr;
+        uint64_t* hk;
+        int32_t *hl, *hr, *hid, *hid_s;
+        DPV_TRY(sc.get(&hk, nr));
+        DPV_TRY(sc.get(&hkey_s, nr));
+        DPV_TRY(sc.get(&hl, nr));
+        DPV_TRY(sc.get(&hr, nr));
+        DPV_TRY(sc.get(&hid, nr));
+        DPV_TRY(sc.get(&hid_s, nr));
+        if (NPD > 0) {
+            k_pair_heads<1><<<grid_for(NPD * 32, B), B, 0, st>>>(
+                NPD, P->rinc_ptr, P->rinc, P->inc_var, P->inc_row, P->n, nullptr, hoff, hk, hl,
+                hr);
             DPV_CHECK_LAUNCH();
-            k_gather_i32<<<grid_for(NPR, B), B, 0, st>>>(NPR, pid_s, pr, P->pair_r);
+        }
+        if (nr > 0) {
+            k_iota<<<grid_for(nr, B), B, 0, st>>>(nr, hid);
+            DPV_CHECK_LAUNCH();
+        }
+        const int eb = bits_for((uint64_t)P->n * (uint64_t)P->n);
+        DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, hk, hkey_s, hid, hid_s, (int)nr, 0, eb,
+                                                   st);
+        }));
+        DPV_TRY(P->alloc(&P->run_l, nr));
+        DPV_TRY(P->alloc(&P->run_r, nr));
+        DPV_TRY(P->alloc(&P->run_len, nr));
+        if (nr > 0) {
+            k_gather_i32<<<grid_for(nr, B), B, 0, st>>>(nr, hid_s, hl, P->run_l);
+            DPV_CHECK_LAUNCH();
+            k_gather_i32<<<grid_for(nr, B), B, 0, st>>>(nr, hid_s, hr, P->run_r);
+            DPV_CHECK_LAUNCH();
+            k_run_extent<<<grid_for(nr * 32, B), B, 0, st>>>(nr, P->I, P->run_l, P->run_r,
+                                                              P->inc_var, P->inc_row, P->run_len);
             DPV_CHECK_LAUNCH();
         }
     }
-    const int64_t NPR = P->NP;
+    const int64_t NRH = P->NR;
 
+    ptimer.lap("before 10. union keys = uni");
     // 10. union keys = unique(hpp ∪ schur ∪ diagonal) (ba.py:201-203)
     uint64_t *hk, *vk;
     int32_t *hc, *vc;
@@ -885,24 +972,35 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_CHECK_LAUNCH();
     }
     {
-        const int64_t tot = NPR + P->n + 3 * P->S + n_extra;
+        // the run heads are sorted by key: unique them (every pair key has a
+        // head), then sort only the short union with the other key sets
+        uint64_t* pk_u;
+        int64_t npu = 0;
+        DPV_TRY(sc.get(&pk_u, std::max<int64_t>(NRH, 1)));
+        if (NRH > 0) {
+            DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+                return cub::DeviceSelect::Unique(t, b, hkey_s, pk_u, dcount, (int)NRH, st);
+            }));
+            DPV_TRY(read_scalar(dcount, &npu, st));
+        }
+        const int64_t tot = npu + P->n + 3 * P->S + n_extra;
         uint64_t *all, *alls, *uk;
         DPV_TRY(sc.get(&all, tot));
         DPV_TRY(sc.get(&alls, tot));
         DPV_TRY(sc.get(&uk, tot));
-        if (NPR > 0)
-            DPV_CUDA(cudaMemcpyAsync(all, pkey_sorted, sizeof(uint64_t) * NPR,
-                                     cudaMemcpyDeviceToDevice, st));
+        if (npu > 0)
+            DPV_CUDA(cudaMemcpyAsync(all, pk_u, sizeof(uint64_t) * npu, cudaMemcpyDeviceToDevice,
+                                     st));
         if (P->n > 0) {
-            k_diag_keys<<<grid_for(P->n, B), B, 0, st>>>(P->n, all + NPR);
+            k_diag_keys<<<grid_for(P->n, B), B, 0, st>>>(P->n, all + npu);
             DPV_CHECK_LAUNCH();
         }
         if (P->S > 0)
-            DPV_CUDA(cudaMemcpyAsync(all + NPR + P->n, hk, sizeof(uint64_t) * 3 * P->S,
+            DPV_CUDA(cudaMemcpyAsync(all + npu + P->n, hk, sizeof(uint64_t) * 3 * P->S,
                                      cudaMemcpyDeviceToDevice, st));
         // sharded global BA: every shard carries the global block pattern
         if (n_extra > 0)
-            DPV_CUDA(cudaMemcpyAsync(all + NPR + P->n + 3 * P->S, extra_keys,
+            DPV_CUDA(cudaMemcpyAsync(all + npu + P->n + 3 * P->S, extra_keys,
                                      sizeof(uint64_t) * n_extra, cudaMemcpyDeviceToDevice, st));
         DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
             return cub::DeviceRadixSort::SortKeys(t, b, all, alls, (int)tot, 0, 64, st);
@@ -932,51 +1030,25 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         k_key_ab<<<grid_for(W, B), B, 0, st>>>(W, P->union_keys, P->n, P->key_a, P->key_b);
         DPV_CHECK_LAUNCH();
     }
-    DPV_TRY(P->alloc(&P->key_pair_ptr, W + 1));
+    // key -> runs CSR (heads sorted by key)
+    DPV_TRY(P->alloc(&P->key_run_ptr, W + 1));
+    if (W > 0) {
+        int64_t* krp;
+        DPV_TRY(sc.get(&krp, W + 1));
+        k_lower_bounds_of<uint64_t, int64_t><<<grid_for(W, B), B, 0, st>>>(
+            W, P->union_keys, hkey_s, NRH, krp);
+        DPV_CHECK_LAUNCH();
+        k_i64_to_i32<<<grid_for(W, B), B, 0, st>>>(W, krp, P->key_run_ptr);
+        DPV_CHECK_LAUNCH();
+    }
     {
-        // key_pair_ptr[w] = lower_bound(sorted pair keys, union_keys[w]); [W] = NP
-        if (W > 0) {
-            k_lower_bounds_of<uint64_t, int64_t><<<grid_for(W, B), B, 0, st>>>(
-                W, P->union_keys, pkey_sorted, NPR, P->key_pair_ptr);
-            DPV_CHECK_LAUNCH();
-        }
-        DPV_CUDA(cudaMemcpyAsync(P->key_pair_ptr + W, &P->NP, sizeof(int64_t),
+        const int32_t nr32 = (int32_t)NRH;
+        DPV_CUDA(cudaMemcpyAsync(P->key_run_ptr + W, &nr32, sizeof(int32_t),
                                  cudaMemcpyHostToDevice, st));
-    }
-
-    // 10b. run-length form of the Schur pairs (banded graphs: ~1 run per key),
-    // so the Schur kernel streams contiguous incidence blocks
-    {
-        int32_t *flag, *rid;
-        DPV_TRY(sc.get(&flag, NPR + 1));
-        DPV_TRY(sc.get(&rid, NPR + 1));
-        k_run_flags<<<grid_for(NPR + 1, B), B, 0, st>>>(NPR, pkey_sorted, P->pair_l, P->pair_r,
-                                                         flag);
-        DPV_CHECK_LAUNCH();
-        DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
-            return cub::DeviceScan::ExclusiveSum(t, b, flag, rid, (int)NPR + 1, st);
-        }));
-        int32_t nr = 0;
-        DPV_CUDA(cudaMemcpyAsync(&nr, rid + NPR, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         DPV_CUDA(cudaStreamSynchronize(st));
-        P->NR = nr;
-        int64_t* run_start;
-        DPV_TRY(sc.get(&run_start, std::max<int64_t>(nr, 1)));
-        DPV_TRY(P->alloc(&P->run_l, nr));
-        DPV_TRY(P->alloc(&P->run_r, nr));
-        DPV_TRY(P->alloc(&P->run_len, nr));
-        DPV_TRY(P->alloc(&P->key_run_ptr, W + 1));
-        if (NPR > 0) {
-            k_run_fill<<<grid_for(NPR, B), B, 0, st>>>(NPR, flag, rid, P->pair_l, P->pair_r,
-                                                        P->run_l, P->run_r, run_start);
-            DPV_CHECK_LAUNCH();
-            k_run_len<<<grid_for(nr, B), B, 0, st>>>(nr, NPR, run_start, P->run_len);
-            DPV_CHECK_LAUNCH();
-        }
-        k_key_runs<<<grid_for(W + 1, B), B, 0, st>>>(W, P->key_pair_ptr, rid, P->key_run_ptr);
-        DPV_CHECK_LAUNCH();
     }
 
+    ptimer.lap("before 10c. grouped Schur c");
     // 10c. grouped Schur complement: depth rows with identical incidence-var
     // lists (all patches of a frame on a banded graph) form a group whose
     // Schur contribution is one SYRK W_g W_g^T on the tensor cores; chunks of
@@ -1080,6 +1152,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         }
     }
 
+    ptimer.lap("before 11. key -> segment C");
     // 11. key -> segment CSR (pose blocks) and var -> segment CSR (rhs_pose)
     {
         const int64_t n3 = 3 * P->S;
@@ -1131,6 +1204,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
                                  cudaMemcpyDeviceToDevice, st));
     }
 
+    ptimer.lap("before 12. system arrays");
     // 12. system arrays
     DPV_TRY(P->alloc(&P->frame_R, (int64_t)P->F * 9));
     DPV_TRY(P->alloc(&P->e_terms, E * 8));
@@ -1162,6 +1236,40 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     DPV_TRY(P->alloc(&P->row_flag, NPD));
     DPV_CUDA(cudaMemsetAsync(P->status, 0, sizeof(int32_t) * 8, st));
     DPV_CUDA(cudaMallocHost(&P->lm_host, sizeof(double) * 16));
+    DPV_CUDA(cudaStreamSynchronize(st));
+    ptimer.lap("12. system arrays");
+    return DPV_OK;
+}
+
+// Lazily materialised Schur pair list (reference order: key-major, rows
+// ascending within a key) for the parity export (ba.py:190-199 maps).
+int32_t ensure_pairs(dpv_problem* P) {
+    if (P->pair_l || P->NP == 0) return DPV_OK;
+    cudaStream_t st = P->alloc_stream;
+    const int B = 256;
+    int64_t *len64, *off;
+    Scratch sc(st);
+    DPV_TRY(sc.get(&len64, P->NR + 1));
+    DPV_TRY(sc.get(&off, P->NR + 1));
+    if (P->NR > 0) {
+        k_i32_to_i64<<<grid_for(P->NR, B), B, 0, st>>>(P->NR, P->run_len, len64);
+        DPV_CHECK_LAUNCH();
+    }
+    DPV_CUDA(cudaMemsetAsync(len64 + P->NR, 0, sizeof(int64_t), st));
+    DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, len64, off, (int)P->NR + 1, st);
+    }));
+    DPV_TRY(P->alloc(&P->pair_l, P->NP));
+    DPV_TRY(P->alloc(&P->pair_r, P->NP));
+    DPV_TRY(P->alloc(&P->key_pair_ptr, P->W + 1));
+    if (P->NR > 0) {
+        k_expand_runs<<<grid_for(P->NR * 32, B), B, 0, st>>>(P->NR, off, P->run_l, P->run_r,
+                                                             P->run_len, P->pair_l, P->pair_r);
+        DPV_CHECK_LAUNCH();
+    }
+    k_key_pair_ptr<<<grid_for(P->W + 1, B), B, 0, st>>>(P->W, P->key_run_ptr, off,
+                                                        P->key_pair_ptr);
+    DPV_CHECK_LAUNCH();
     DPV_CUDA(cudaStreamSynchronize(st));
     return DPV_OK;
 }

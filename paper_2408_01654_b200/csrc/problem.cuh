@@ -219,6 +219,7 @@ int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const doubl
              int w1, int levels, int radius, int dtype, float* out, cudaStream_t st);
 int32_t proximity_detect(const double* centers, int64_t n, int64_t gap, double thr,
                          int64_t* pairs, int64_t cap, int64_t* count, cudaStream_t st);
+int32_t ensure_pairs(dpv_problem* P);
 int32_t coords_sel(dpv_problem* p, const double* q, const double* t, const double* d,
                    double scale, const int64_t* sel, int64_t n_sel, double* out,
                    cudaStream_t st);
