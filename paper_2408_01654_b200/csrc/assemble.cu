@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
     const double* __restrict__ a_w, const double* __restrict__ r_ray,
     const double* __restrict__ Rall, const double* __restrict__ tall,
     const double* __restrict__ d, double fx, double fy, double cx, double cy,
-    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g) {
+    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g,
+    double* __restrict__ seg_obj) {
     const double intr[4] = {fx, fy, cx, cy};
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
         }
         __syncwarp();
         double H[21], G[6];
+        double fobj = 0.0;     // sum w r^2 over the segment (ba.py:248-253), free here
 #pragma unroll
         for (int k = 0; k < 21; ++k) H[k] = 0.0;
 #pragma unroll
@@ -426,6 +428,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
                     }
                     cdd += wjd * jd[r];
                     gd += wjd * rr[r];
+                    fobj += wv[r] * rr[r] * rr[r];
                 }
             }
 #pragma unroll
@@ -440,6 +443,8 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
         for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
 #pragma unroll
         for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
+        fobj = warp_sum(fobj);
+        if (seg_obj && lane == 0) seg_obj[s] = fobj;
         if (lane < 21) {
             double v = 0.0;
 #pragma unroll
@@ -837,12 +842,13 @@ int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cu
     return DPV_OK;
 }
 
-int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
-                 cudaStream_t st) {
+// K2+K3 edge pass at (q, t, d): per-edge terms, per-segment Gram sums and,
+// when obj != nullptr, the objective at that state (fixed-order sum of the
+// per-segment sums) - the LM driver evaluates every candidate this way, so an
+// accepted candidate's edge pass is already done (speculative assembly).
+int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, const double* d,
+                            double* obj, cudaStream_t st) {
     DPV_TRY(frame_rotations(p, q, st));
-    DPV_CUDA(cudaMemsetAsync(p->scal, 0, sizeof(double) * 8, st));
-    auto* grad_bits = reinterpret_cast<unsigned long long*>(p->scal);
-    auto* n_inactive = reinterpret_cast<unsigned long long*>(p->scal + 6);
     if (p->S > 0) {
         DPV_ARG(p->m == 9, "assembly kernel is instantiated for 3x3 patches");
         const int warps_per_block = 4;
@@ -854,7 +860,7 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
     k_assemble_edges<9, U, B, PF><<<blocks, 32 * warps_per_block, 0, st>>>(                    \
         p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,        \
         p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
-        p->e_terms, p->seg_h, p->seg_g)
+        p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr)
         switch (variant) {
             case 1: DPV_ASM(3, 3, false); break;
             case 2: DPV_ASM(1, 3, true); break;
@@ -864,6 +870,24 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
 #undef DPV_ASM
         DPV_CHECK_LAUNCH();
     }
+    if (obj) {
+        if (p->S > 0) {
+            DPV_TSTART("sum_parts", st);
+            k_sum_parts<<<1, 1024, 0, st>>>((int)p->S, p->seg_obj, obj);
+            DPV_CHECK_LAUNCH();
+        } else {
+            DPV_CUDA(cudaMemsetAsync(obj, 0, sizeof(double), st));
+        }
+    }
+    return DPV_OK;
+}
+
+// the rest of the assembly (rows, incidences, Schur, rhs, pin) from the
+// edge pass's terms; t = the state's translations (scale pin)
+int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
+    DPV_CUDA(cudaMemsetAsync(p->scal, 0, sizeof(double) * 8, st));
+    auto* grad_bits = reinterpret_cast<unsigned long long*>(p->scal);
+    auto* n_inactive = reinterpret_cast<unsigned long long*>(p->scal + 6);
     if (p->P > 0) {
         DPV_TSTART("rows", st);
         k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,
@@ -926,6 +950,12 @@ int32_t assemble(dpv_problem* p, const double* q, const double* t, const double*
         }
     }
     return DPV_OK;
+}
+
+int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
+                 cudaStream_t st) {
+    DPV_TRY(assemble_edges_pass(p, q, t, d, nullptr, st));
+    return assemble_rest(p, t, st);
 }
 
 }  // namespace dpv

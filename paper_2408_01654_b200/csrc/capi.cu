@@ -568,7 +568,14 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     if (P) DPV_CUDA(cudaMemcpyAsync(wd, d, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
     double* h = p->lm_host;  // pinned: [0] obj, [1] status, [2] step norm, [3] grad, [4] inact
     double* dev_scalar = p->scal + 8;  // scal[8..15] LM scalars on the device
-    DPV_TRY(objective(p, wq, wt, wd, dev_scalar, st));
+    // speculative assembly: every state's objective comes from its edge pass,
+    // so the accepted candidate's pass is the next iteration's (ba.py:534-605
+    // control flow unchanged; DPV_LM_PLAIN=1: separate objective kernel)
+    static const bool plain = getenv("DPV_LM_PLAIN") && atoi(getenv("DPV_LM_PLAIN")) != 0;
+    if (plain)
+        DPV_TRY(objective(p, wq, wt, wd, dev_scalar, st));
+    else
+        DPV_TRY(assemble_edges_pass(p, wq, wt, wd, dev_scalar, st));
     DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
     DPV_CUDA(cudaStreamSynchronize(st));
     double obj = h[0];
@@ -580,7 +587,8 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     int32_t* status = p->status;
     for (int it = 0; it < params->max_iterations; ++it) {
         const double tic = now_s();
-        DPV_TRY(assemble(p, wq, wt, wd, st));
+        if (plain) DPV_TRY(assemble(p, wq, wt, wd, st));
+        else DPV_TRY(assemble_rest(p, wt, st));     // edge pass done when wq was evaluated
         DPV_CUDA(cudaMemcpyAsync(h + 3, p->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
         DPV_CUDA(cudaMemcpyAsync(h + 4, p->scal + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
         bool accepted = false, solved_once = false, singular = false;
@@ -591,7 +599,10 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
             rep->n_attempts++;
             DPV_TRY(solve(p, lam, p->lm_dp, p->lm_dd, status, st));
             DPV_TRY(apply_step(p, wq, wt, wd, p->lm_dp, p->lm_dd, p->lm_q, p->lm_t, p->lm_d, st));
-            DPV_TRY(objective(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
+            if (plain)
+                DPV_TRY(objective(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
+            else
+                DPV_TRY(assemble_edges_pass(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
             k_step_norm<<<1, 256, 0, st>>>(6 * p->n, p->lm_dp, P, p->lm_dd, dev_scalar + 1);
             DPV_CHECK_LAUNCH();
             DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -1210,6 +1210,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     DPV_TRY(P->alloc(&P->e_terms, E * 8));
     DPV_TRY(P->alloc(&P->seg_h, P->S * 21));
     DPV_TRY(P->alloc(&P->seg_g, P->S * 6));
+    DPV_TRY(P->alloc(&P->seg_obj, P->S));
     DPV_TRY(P->alloc(&P->depth_diag, NPD));
     DPV_TRY(P->alloc(&P->rhs_depth, NPD));
     DPV_TRY(P->alloc(&P->active, NPD));

@@ -129,6 +129,7 @@ struct dpv_problem {
     double* e_terms = nullptr;     // (E, 8): e_pd[6], c_dd, g_d
     double* seg_h = nullptr;       // (S, 21) upper-triangular sum of J^T W J
     double* seg_g = nullptr;       // (S, 6)  sum of J^T W r
+    double* seg_obj = nullptr;     // (S) sum of w r^2 (LM candidate objective)
     double* depth_diag = nullptr;  // (P)
     double* rhs_depth = nullptr;   // (P)
     uint8_t* active = nullptr;     // (P)
@@ -153,6 +154,7 @@ struct dpv_problem {
     dpv::FactorPlan* plan = nullptr;  // tile plan of the reduced system (lazily built)
     int32_t* perm_pos = nullptr;   // (n) pose var -> permuted position in the dense solve
     dpv::SpdPlan* spd = nullptr;   // sparse band+border solver plan (lazily built)
+    int32_t spd_failed = 0;        // plan impossible -> tile-plan factorisation
     double* sblk = nullptr;        // (W, 36) S(lambda) blocks for the sparse solver
     int32_t* status = nullptr;     // (4) device flags
 
@@ -208,6 +210,9 @@ int32_t residuals(dpv_problem* p, const double* q, const double* t, const double
                   double* res, uint8_t* valid, cudaStream_t st);
 int32_t assemble(dpv_problem* p, const double* q, const double* t, const double* d,
                  cudaStream_t st);
+int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, const double* d,
+                            double* obj, cudaStream_t st);
+int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st);
 int32_t coords(dpv_problem* p, const double* q, const double* t, const double* d, double scale,
                double* out, cudaStream_t st);
 int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cudaStream_t st);

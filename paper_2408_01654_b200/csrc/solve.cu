@@ -323,7 +323,7 @@ int32_t ensure_plan(dpv_problem* p, int64_t N, cudaStream_t st) {
     std::vector<int32_t> pos(n);
     for (int64_t v = 0; v < n; ++v) pos[v] = (int32_t)v;
     const char* env = getenv("DPV_DENSE_SOLVE");
-    const bool dense = env && atoi(env) == 1;   // 2: sparse tile plan
+    const bool dense = env && atoi(env) == 1;   // 2 (or spd fallback): sparse tile plan
     auto* plan = new (std::nothrow) FactorPlan();
     DPV_ARG(plan != nullptr, "allocation failed");
     if (dense) {
@@ -423,7 +423,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
                                              p->schur_blocks, p->rhs_pose, p->rhs_schur, p->scal,
                                              lam, dp, status);
         DPV_CHECK_LAUNCH();
-    } else if (!dense_solve_forced()) {
+    } else if (!dense_solve_forced() && !p->spd_failed) {
         // banded + border sparse factorisation (spd.cu)
         if (!p->spd) {
             std::vector<int32_t> ka(p->W), kb(p->W);
@@ -432,7 +432,14 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
             DPV_CUDA(cudaMemcpyAsync(kb.data(), p->key_b, sizeof(int32_t) * p->W,
                                      cudaMemcpyDeviceToHost, st));
             DPV_CUDA(cudaStreamSynchronize(st));
-            DPV_TRY(spd_plan_build(ka.data(), kb.data(), p->W, p->n, &p->spd, st));
+            if (spd_plan_build(ka.data(), kb.data(), p->W, p->n, &p->spd, st) != DPV_OK) {
+                // e.g. a border too large for one co-resident factor grid: the
+                // tile-plan factorisation below handles any pattern
+                clear_error();
+                p->spd = nullptr;
+                p->spd_failed = 1;
+                return solve(p, lam, dp, dd, status, st);
+            }
             DPV_TRY(p->alloc(&p->sblk, p->W * 36));
         }
         DPV_TRY(reduced_system(p, lam, p->sblk, p->red_rhs, nullptr, st));

@@ -194,3 +194,17 @@ def test_grouped_schur_matches_golden(golden, case, monkeypatch):
     sys_ = ba.assemble(prob)
     close(sys_.schur_blocks, z[pp + "sys_schur_blocks"], 1e-9, 1e-9)
     close(sys_.rhs_schur, z[pp + "sys_rhs_schur"], 1e-9, 1e-9)
+
+
+def test_lm_solve_tile_plan_fallback(golden, monkeypatch):
+    """When the banded+border plan is impossible (forced here with
+    DPV_SPD_FAIL) the solve falls back to the tile-plan factorisation and the
+    LM trajectory is unchanged (block-sparse golden problem, 60 poses)."""
+    monkeypatch.setenv("DPV_SPD_FAIL", "1")
+    z = golden("loops")
+    g, prob = make(z, "g_", "p_")
+    rep = ba.solve(prob, int(z["p_lm_iters"]), float(z["p_lm_tol"]),
+                   backend_threshold=int(z["p_lm_threshold"]))
+    assert rep.iterations == int(z["p_rep_iterations"])
+    assert rep.final_objective == pytest.approx(float(z["p_rep_final"]), rel=1e-6, abs=1e-10)
+    close(g.soa()["frame_t"], z["p_after_frame_t"], 1e-7, 1e-9)
