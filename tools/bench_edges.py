@@ -68,6 +68,8 @@ def main():
         tm = _lib.timing_collect()
         _lib.timing_enable(False)
         kb = tm.get("key_blocks", (0, 1))
+        vs = tm.get("var_schur", (0, 1))
+        print(f"    var_schur {vs[0] / vs[1]:.3f} ms")
         gs = tm.get("group_syrk", (0, 1))
         print(f"key variant {v}: chain {ms:.3f} ms, k_key_blocks {kb[0] / kb[1]:.3f} ms, group_syrk {gs[0] / gs[1]:.3f} ms")
 
