@@ -76,51 +76,62 @@ def measured_peaks():
 
 
 class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML polling thread (1 ms period; the timed region of a cfg3
+    run is only ~40 ms, below nvidia-smi's sampling period); nvidia-smi as a
+    fallback when NVML is unavailable."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
     def __init__(self, index=0):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.thread = None
+        self.nvml = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+    def _poll(self):
+        p = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = p.nvmlDeviceGetClockInfo(self.handle, p.NVML_CLOCK_SM)
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[5 + i].lower() in ("active", "1")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        p = self.nvml
+        reasons = sorted({name for _, rs in self.rows for name, attr in self.NAMES
+                          if hasattr(p, attr) and rs & getattr(p, attr)})
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.max_sm),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 1 ms polling"}
 
 
 # ---------------------------------------------------------------------------
@@ -323,9 +334,15 @@ def kernel_rooflines(timing, work, steps, hbm_peak):
         "incidences": ("hbm", 2 * E * (4 + 48) + I * 96, "B"),
         # Schur pair products on DMMA: 72 flop per pair (6x6 outer product)
         "key_blocks": ("tensor", int(info.n_pairs) * 72.0, "flop"),
-        # band+border factorisation on DMMA (the plan's tile products)
+        # band+border factorisation on DMMA (the plan's tile products, both levels)
         "spd_factor": ("tensor", plan.get("update_flops", 0.0), "flop"),
     }
+    # one entry per kernel FUNCTION (as in the ncu launch list): the two
+    # levels of the sparse factorisation are the same k_spd_factor
+    timing = dict(timing)
+    if "spd_factor2" in timing:
+        a, b = timing.get("spd_factor", (0.0, 0)), timing.pop("spd_factor2")
+        timing["spd_factor"] = (a[0] + b[0], a[1] + b[1])
     for name, (ms, cnt) in timing.items():
         rec = {"ms_per_step": ms / steps, "launches_per_step": cnt / steps}
         if name in per_step and per_step[name][1] > 0:
