@@ -163,6 +163,14 @@ int32_t dpv_objective(dpv_problem* prob, const double* q, const double* t, const
  * reductions + Schur elimination into the handle's system arrays. */
 int32_t dpv_assemble(dpv_problem* prob, const double* q, const double* t, const double* d,
                      void* stream);
+/* dpv_assemble in two halves (the native LM's speculative assembly):
+ * the per-edge pass at (q, t, d) - K2+K3 terms and per-segment sums, plus the
+ * objective at that state into objective_out (DEVICE f64, may be NULL) - and
+ * the rest (depth rows, incidences, Schur blocks, rhs, gauge pin) from the
+ * last edge pass.  dpv_assemble == dpv_assemble_edges + dpv_assemble_rest. */
+int32_t dpv_assemble_edges(dpv_problem* prob, const double* q, const double* t, const double* d,
+                           double* objective_out, void* stream);
+int32_t dpv_assemble_rest(dpv_problem* prob, const double* t, void* stream);
 /* BlockSparseSystem.reduced_system(lam) (ba.py:303-319). Any output may be NULL. */
 int32_t dpv_reduced_system(dpv_problem* prob, double lam, double* blocks, double* rhs,
                            double* cinv, void* stream);

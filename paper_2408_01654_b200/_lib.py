@@ -78,6 +78,8 @@ SIGNATURES = {
     "dpv_residuals": (C.c_int32, [vp, vp, vp, vp, vp, vp, vp]),
     "dpv_objective": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
     "dpv_assemble": (C.c_int32, [vp, vp, vp, vp, vp]),
+    "dpv_assemble_edges": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
+    "dpv_assemble_rest": (C.c_int32, [vp, vp, vp]),
     "dpv_reduced_system": (C.c_int32, [vp, C.c_double, vp, vp, vp, vp]),
     "dpv_solve": (C.c_int32, [vp, C.c_double, vp, vp, vp, vp]),
     "dpv_back_substitute": (C.c_int32, [vp, C.c_double, vp, vp, vp]),

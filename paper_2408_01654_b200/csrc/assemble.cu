@@ -206,6 +206,23 @@ __global__ void __launch_bounds__(256, MINB) k_objective_seg(
     }
 }
 
+// block b sums the contiguous slice [b*n/B, (b+1)*n/B) in a fixed order
+__global__ void k_slice_sums(int64_t n, const double* v, double* part) {
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = (int64_t)blockIdx.x * per, hi = min(n, lo + per);
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += v[i];
+    __shared__ double sh[32];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
 __global__ void k_sum_parts(int n, const double* part, double* out) {
     __shared__ double sh[32];
     double acc = 0.0;
@@ -872,8 +889,13 @@ int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, co
     }
     if (obj) {
         if (p->S > 0) {
+            // fixed-order two-level sum: contiguous slices per block, then the
+            // block partials (deterministic)
+            const int nb = (int)std::min<int64_t>(kObjBlocks, (p->S + 255) / 256);
             DPV_TSTART("sum_parts", st);
-            k_sum_parts<<<1, 1024, 0, st>>>((int)p->S, p->seg_obj, obj);
+            k_slice_sums<<<nb, 256, 0, st>>>(p->S, p->seg_obj, p->obj_part);
+            DPV_CHECK_LAUNCH();
+            k_sum_parts<<<1, 1024, 0, st>>>(nb, p->obj_part, obj);
             DPV_CHECK_LAUNCH();
         } else {
             DPV_CUDA(cudaMemsetAsync(obj, 0, sizeof(double), st));

@@ -507,6 +507,19 @@ int32_t dpv_reduced_system(dpv_problem* p, double lam, double* blocks, double* r
     return reduced_system(p, lam, blocks, rhs, cinv, as_stream(stream));
 }
 
+int32_t dpv_assemble_edges(dpv_problem* p, const double* q, const double* t, const double* d,
+                           double* objective_out, void* stream) {
+    clear_error();
+    DPV_ARG(p && q && t && (d || p->P == 0), "NULL argument");
+    return assemble_edges_pass(p, q, t, d, objective_out, as_stream(stream));
+}
+
+int32_t dpv_assemble_rest(dpv_problem* p, const double* t, void* stream) {
+    clear_error();
+    DPV_ARG(p && t, "NULL argument");
+    return assemble_rest(p, t, as_stream(stream));
+}
+
 int32_t dpv_solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status_dev,
                   void* stream) {
     clear_error();
