@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-global", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--batch-seqs", type=int, default=8)
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: multi-rank tests on one GPU)")
@@ -559,12 +561,17 @@ def run_ours(args):
     # global loop-closure BA (loop.close: new BAProblem + solve(8 iters, 1e-9))
     glob = None
     window = None
+    batch = None
     if not args.no_global and world == 1:
         glob = run_global(work, args, torch)
         try:
             window = run_window(args, torch)
         except Exception as exc:     # reported, not fatal for the headline
             window = {"error": repr(exc)}
+        try:
+            batch = None if args.no_batch else run_batch(args, torch, n_seq=args.batch_seqs)
+        except Exception as exc:
+            batch = {"error": repr(exc)}
     elif not args.no_global:
         t0 = time.perf_counter()
         rep, *_ = work["prob"].solve(max_iterations=args.lm_iters, tolerance=1e-9)
@@ -608,6 +615,7 @@ def run_ours(args):
         "index_build_ms": work["build_ms"],
         "global_ba": glob,
         "window_step": window,
+        "batch_replicas": batch,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -745,6 +753,112 @@ def run_window(args, torch, reps=5):
             "E": E, "ms": ms, "value": 2 * E / (ms * 1e-3), "unit": "patch-edges/s (x2 LM iters)",
             "iterations": rep.iterations, "final_objective": rep.final_objective,
             "includes": "index build, correlation, native LM, write-back (wall clock, synced)"}
+
+
+def run_batch(args, torch, n_seq=8, reps=5, threads=0):
+    """cfg5: n_seq independent TartanAir-shape sequences on
+    this GPU as replicas.  One batch step = for every sequence a new 22-frame
+    BAProblem, the correlation of its window edges (2 levels, bf16) and
+    solve(2 LM iterations, tol 1e-12), as the cfg2 window step; the problems
+    run concurrently (ba.build_batch / ba.solve_batch: one stream and host
+    worker each, no collective).  Also times the same steps run one after
+    another, for the batching gain."""
+    from paper_2408_01654_b200 import _lib, ba, corr, synthetic
+    seqs = []
+    C = args.channels
+    fdt = torch.bfloat16 if args.feat_dtype == "bf16" else torch.float32
+    for s in range(n_seq):
+        scene, graph, free = synthetic.make_config("cfg5", seed=s)
+        w, h = scene.spec.image_size
+        gen = torch.Generator(device="cuda").manual_seed(100 + s)
+        fmap = (torch.randn((graph.n_frames, h // 4, w // 4, C), generator=gen, device="cuda")
+                / math.sqrt(C)).to(fdt)
+        gmap = (torch.randn((graph.n_patches, 9, C), generator=gen, device="cuda")
+                / math.sqrt(C)).to(fdt)
+        seqs.append(dict(graph=graph, free=free, pyr=corr.pyramid(fmap), gmap=gmap,
+                         soa0={k: np.array(v) for k, v in graph.soa().items()}))
+
+    def reset():
+        for sq in seqs:
+            g = sq["graph"]
+            g._q.view[:] = sq["soa0"]["frame_q"]
+            g._t.view[:] = sq["soa0"]["frame_t"]
+            g._depth.view[:] = sq["soa0"]["patch_depth"]
+            g._pose_ver += 1
+            g._patch_ver += 1
+            g.device()
+        torch.cuda.synchronize()
+
+    def window_corr(sq, prob):
+        h_ = prob._ensure()
+        E = int(prob.info().n_edges)
+        q, t, d = prob.device_state()
+        mir = sq["graph"].device()
+        eidx = prob.view("edge_idx")
+        sel = torch.arange(E, dtype=torch.int64, device="cuda")
+        coords = torch.empty((E, 9, 2), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().dpv_reproject_coords_sel(h_, _lib.ptr(q), _lib.ptr(t), _lib.ptr(d),
+                                                       0.25, _lib.ptr(sel), E, _lib.ptr(coords),
+                                                       _lib.stream_ptr()), "coords")
+        corr.corr(sq["gmap"], sq["pyr"], coords, mir["edge_gpatch"][eidx].to(torch.int32),
+                  mir["edge_dst"][eidx].to(torch.int32))
+        return E
+
+    phases = {"build": [], "corr": [], "solve": []}
+
+    streams = [torch.cuda.Stream() for _ in seqs]      # one per sequence, reused
+
+    def batched():
+        t0 = time.perf_counter()
+        probs = [ba.BAProblem(sq["graph"], sq["free"]) for sq in seqs]
+        ba.build_batch(probs, threads, streams=streams)
+        t1 = time.perf_counter()
+        E = 0
+        for sq, p in zip(seqs, probs):
+            with torch.cuda.stream(p._stream):
+                E += window_corr(sq, p)
+        t2 = time.perf_counter()
+        reps_ = ba.solve_batch(probs, 2, 1e-12, threads=threads)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        for k, v in zip(phases, (t1 - t0, t2 - t1, t3 - t2)):
+            phases[k].append(v * 1e3)
+        return E, reps_
+
+    def sequential():
+        E = 0
+        for sq in seqs:
+            p = ba.BAProblem(sq["graph"], sq["free"])
+            E += window_corr(sq, p)
+            ba.solve(p, 2, 1e-12)
+        torch.cuda.synchronize()
+        return E
+
+    tb, ts = [], []
+    E = 0
+    out = []
+    for r in range(reps + 2):
+        reset()
+        t0 = time.perf_counter()
+        E, out = batched()
+        if r >= 2:
+            tb.append((time.perf_counter() - t0) * 1e3)
+        reset()
+        t0 = time.perf_counter()
+        sequential()
+        if r >= 2:
+            ts.append((time.perf_counter() - t0) * 1e3)
+    ms, ms_seq = float(np.median(tb)), float(np.median(ts))
+    bad = [type(x).__name__ for x in out if isinstance(x, Exception)]
+    return {"config": "cfg5: " + synthetic.DESCRIPTIONS["cfg5"], "sequences": n_seq,
+            "E_total": E, "ms_per_batch": ms, "window_steps_per_s": n_seq / (ms * 1e-3),
+            "value": 2 * E / (ms * 1e-3), "unit": "patch-edges/s (x2 LM iters)",
+            "sequential_ms": ms_seq, "batching_gain": ms_seq / ms,
+            "phase_ms": {k: float(np.median(v[2:])) for k, v in phases.items()},
+            "iterations": [x.iterations for x in out if not isinstance(x, Exception)],
+            "failed": bad,
+            "includes": "index build, correlation, native LM, write-back for every sequence "
+                        "(wall clock, synced); replicas on one stream + host worker each"}
 
 
 def run_global(work, args, torch):

@@ -229,6 +229,23 @@ typedef struct dpv_lm_report {  /* ba.BAReport (ba.py:497-518) */
 int32_t dpv_lm_solve(dpv_problem* prob, double* q, double* t, double* d,
                      const dpv_lm_params* params, dpv_lm_report* report, void* stream);
 
+/* Batched replicas: `count` independent problems,
+ * each on its own stream, driven concurrently by up to `threads` host workers
+ * (<= 0: one per hardware thread).  Element i of every array belongs to
+ * problem i; status[i] is that problem's own return code (a singular problem
+ * does not stop the others).  Returns DPV_OK, or the first failing problem's
+ * code with dpv_last_error() naming it.  No reference counterpart: the
+ * reference solves one problem per ba.solve call (ba.py:534-605), and these
+ * are exactly `count` such calls. */
+int32_t dpv_problem_create_batch(int32_t count, const dpv_graph* graphs,
+                                 const int32_t* first_free, const int32_t* last_free,
+                                 void* const* streams, int32_t threads, dpv_problem** out,
+                                 int32_t* status);
+int32_t dpv_lm_solve_batch(int32_t count, dpv_problem* const* probs, double* const* q,
+                           double* const* t, double* const* d, const dpv_lm_params* params,
+                           dpv_lm_report* reports, void* const* streams, int32_t threads,
+                           int32_t* status);
+
 /* Block-sparse SPD solve (the block-sparse backend, block_cholesky.py:48-111
  * + BlockCholeskyFactor.solve 31-45): keys (n_keys, 2) HOST int64 upper
  * pattern a <= b of 6x6 blocks; blocks (n_keys, 6, 6) and rhs (6n) DEVICE

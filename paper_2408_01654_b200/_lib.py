@@ -86,6 +86,8 @@ SIGNATURES = {
     "dpv_apply_step": (C.c_int32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "dpv_lm_solve": (C.c_int32, [vp, vp, vp, vp, C.POINTER(DpvLmParams),
                                  C.POINTER(DpvLmReport), vp]),
+    "dpv_problem_create_batch": (C.c_int32, [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp]),
+    "dpv_lm_solve_batch": (C.c_int32, [C.c_int32, vp, vp, vp, vp, vp, vp, vp, C.c_int32, vp]),
     "dpv_cholesky_solve": (C.c_int32, [vp, vp, C.c_int64, vp, vp]),
     "dpv_block_sparse_solve": (C.c_int32, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
     "dpv_problem_spd_info": (C.c_int32, [vp, c_int64_p]),

@@ -92,11 +92,8 @@ class BAProblem:
 
     # -- device handle ---------------------------------------------------------
 
-    def _ensure(self):
-        if self._handle is not None:
-            return self._handle
-        torch = _torch()
-        lib = _lib.lib()
+    def _graph_view(self):
+        """The graph's device mirror as the C-ABI's dpv_graph view."""
         mir = self._g.device()
         g = _lib.DpvGraph()
         g.n_frames = self._g.n_frames
@@ -111,6 +108,14 @@ class BAProblem:
         g.edge_conf = mir["edge_conf"].data_ptr() if g.n_edges else 0
         for i, v in enumerate(self._g.intrinsics.as_array()):
             g.intr[i] = float(v)
+        return g
+
+    def _ensure(self):
+        if self._handle is not None:
+            return self._handle
+        torch = _torch()
+        lib = _lib.lib()
+        g = self._graph_view()
         eidx = None
         if self._given is not None:
             if len(self._given) and (self._given.min() < 0 or self._given.max() >= g.n_edges):
@@ -603,3 +608,104 @@ def solve(problem: BAProblem, max_iterations: int = 50, tolerance: float = 1e-9,
     rep = solve_device(problem, q, t, d, max_iterations, tolerance, backend, backend_threshold)
     problem.write_back(q, t, d)
     return rep
+
+
+# ---------------------------------------------------------------------------
+# batched replicas: many independent problems
+
+
+def build_batch(problems, threads: int = 0, streams=None) -> None:
+    """Build the device index of every problem concurrently (one stream and
+    one host worker per problem, dpv_problem_create_batch).  Same index as
+    building each problem alone; problems with a handle already are skipped,
+    as are those with explicit edge_indices (built one by one).  ``streams``:
+    one torch stream per problem (reused streams keep the caching allocator
+    warm); the problem keeps its stream for later work."""
+    torch = _torch()
+    todo = [p for p in problems if p._handle is None and p._given is None]
+    for p in problems:
+        if p._handle is None and p._given is not None:
+            p._ensure()
+    if not todo:
+        return
+    n = len(todo)
+    graphs = (_lib.DpvGraph * n)(*[p._graph_view() for p in todo])
+    first = (C.c_int32 * n)(*[p.first_free for p in todo])
+    last = (C.c_int32 * n)(*[p.last_free for p in todo])
+    if streams is None:
+        streams = [torch.cuda.Stream() for _ in todo]
+    else:
+        streams = [s for p, s in zip(problems, streams) if p in todo]
+    torch.cuda.current_stream().synchronize()      # graph mirrors are ready
+    sp = (C.c_void_p * n)(*[s.cuda_stream for s in streams])
+    out = (C.c_void_p * n)()
+    status = (C.c_int32 * n)()
+    rc = _lib.lib().dpv_problem_create_batch(n, graphs, first, last, sp, int(threads), out,
+                                              status)
+    for i, p in enumerate(todo):          # keep every handle that was built
+        if out[i]:
+            p._handle = C.c_void_p(out[i])
+            p._stream = streams[i]          # the handle frees on its build stream
+            info = _lib.DpvProblemInfo()
+            _lib.check(_lib.lib().dpv_problem_get_info(p._handle, C.byref(info)), "problem info")
+            p._info = info
+    _lib.check(rc, "build_batch")
+
+
+def solve_batch(problems, max_iterations: int = 50, tolerance: float = 1e-9,
+                backend: str | None = None, backend_threshold: int = DEFAULT_BACKEND_THRESHOLD,
+                threads: int = 0) -> list:
+    """``[solve(p, ...) for p in problems]`` run as concurrent replicas: every
+    problem's native LM (ba.py:534-605) on its own stream and host worker
+    (dpv_lm_solve_batch).  Returns one entry per problem: its BAReport, or the
+    SingularSystem instance where ``solve`` would have raised (that problem's
+    graph is then left unwritten, as in ``solve``).  max_iterations, tolerance
+    and backend_threshold may be scalars or one value per problem."""
+    torch = _torch()
+    build_batch(problems, threads)
+    n = len(problems)
+    if n == 0:
+        return []
+
+    def per(v):
+        return list(v) if isinstance(v, (list, tuple, np.ndarray)) else [v] * n
+    iters, tols, thresholds = per(max_iterations), per(tolerance), per(backend_threshold)
+    if not (len(iters) == len(tols) == len(thresholds) == n):
+        raise ValueError("per-problem settings must have one entry per problem")
+    chosen = [backend or select_backend(p, th) for p, th in zip(problems, thresholds)]
+    for c in chosen:
+        if c not in _BACKENDS:
+            raise KeyError(c)
+    active = [p.active_patch_count() for p in problems]
+    states = [p.device_state() for p in problems]
+    streams = [getattr(p, "_stream", None) or torch.cuda.Stream() for p in problems]
+    torch.cuda.current_stream().synchronize()      # states are ready
+    hs = (C.c_void_p * n)(*[p._ensure().value for p in problems])
+    qs = (C.c_void_p * n)(*[s[0].data_ptr() for s in states])
+    ts = (C.c_void_p * n)(*[s[1].data_ptr() for s in states])
+    ds = (C.c_void_p * n)(*[s[2].data_ptr() for s in states])
+    params = (_lib.DpvLmParams * n)(*[_lib.DpvLmParams(int(it), float(tol), float(p.damping))
+                                       for p, it, tol in zip(problems, iters, tols)])
+    reps = (_lib.DpvLmReport * n)()
+    sp = (C.c_void_p * n)(*[s.cuda_stream for s in streams])
+    status = (C.c_int32 * n)()
+    rc = _lib.lib().dpv_lm_solve_batch(n, hs, qs, ts, ds, params, reps, sp, int(threads), status)
+    if rc not in (_lib.DPV_OK, _lib.DPV_SINGULAR):
+        _lib.check(rc, "solve_batch")
+    out = []
+    for i, p in enumerate(problems):
+        if status[i] == _lib.DPV_SINGULAR:
+            out.append(SingularSystem(f"solve_batch: problem {i}: matrix not positive definite"))
+            continue
+        if status[i] != _lib.DPV_OK:
+            _lib.check(status[i], f"solve_batch problem {i}")
+        r = reps[i]
+        out.append(BAReport(int(r.iterations), r.initial_objective, r.final_objective, chosen[i],
+                            iteration_times=[r.iteration_times[k] for k in range(r.times_len)],
+                            converged=bool(r.converged), gradient_norm=r.gradient_norm,
+                            unconstrained_depths=int(r.unconstrained_depths),
+                            active_patches=int(active[i]), final_damping=r.final_damping,
+                            step_norm=r.step_norm, n_attempts=int(r.n_attempts)))
+        p.damping = r.final_damping
+        p.write_back(*states[i])
+    return out

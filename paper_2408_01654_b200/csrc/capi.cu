@@ -4,6 +4,7 @@
 #include <cstring>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -57,21 +58,24 @@ void timer_push(const char* name, cudaStream_t st, bool start) {
 }
 
 int32_t configure_pool() {
-    static bool done = false;
-    if (done) return DPV_OK;
+    static std::atomic<bool> done{false};
+    static std::mutex mu;
+    if (done.load(std::memory_order_acquire)) return DPV_OK;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.load(std::memory_order_relaxed)) return DPV_OK;
     int dev = 0;
     DPV_CUDA(cudaGetDevice(&dev));
     cudaMemPool_t pool;
     DPV_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t keep = UINT64_MAX;
     DPV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    done = true;
+    done.store(true, std::memory_order_release);
     return DPV_OK;
 }
 
 int sm_count() {
-    static int cached = 0;
-    if (cached == 0) {
+    static std::atomic<int> cached{0};
+    if (cached.load(std::memory_order_relaxed) == 0) {
         int dev = 0, v = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -858,6 +862,84 @@ int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, 
                 (dtype == 0 || dtype == 1),
             "bad avg_pool4 args");
     return avg_pool4(fmap, n_frames, h, w, channels, dtype, out, as_stream(stream));
+}
+
+}  // extern "C"
+
+// ---- batched replicas (SURVEY 8(d) cfg5, 8(e) "replicas only") ----------------
+// Independent problems (one per sequence) run concurrently: one host worker
+// per problem slot, each driving its problem on its own stream, so the
+// latency-bound index builds and LM iterations of many small windows overlap
+// on the device.  No collective and no state shared between problems.
+
+namespace dpv {
+namespace {
+template <typename Fn>
+void run_workers(int32_t count, int32_t threads, Fn fn) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (threads <= 0) threads = (int32_t)std::max(1u, std::thread::hardware_concurrency());
+    threads = std::max(1, std::min(threads, count));
+    std::atomic<int32_t> next{0};
+    auto work = [&]() {
+        cudaSetDevice(dev);
+        for (int32_t i = next.fetch_add(1); i < count; i = next.fetch_add(1)) fn(i);
+    };
+    std::vector<std::thread> pool;
+    pool.reserve(threads - 1);
+    for (int32_t k = 1; k < threads; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+}
+
+// the first failing problem's status and message become the call's
+int32_t first_failure(int32_t count, const int32_t* status, const std::vector<std::string>& msg) {
+    for (int32_t i = 0; i < count; ++i)
+        if (status[i] != DPV_OK) {
+            set_error("problem " + std::to_string(i) + ": " + msg[i]);
+            return status[i];
+        }
+    return DPV_OK;
+}
+}  // namespace
+}  // namespace dpv
+
+extern "C" {
+
+int32_t dpv_problem_create_batch(int32_t count, const dpv_graph* graphs,
+                                 const int32_t* first_free, const int32_t* last_free,
+                                 void* const* streams, int32_t threads, dpv_problem** out,
+                                 int32_t* status) {
+    clear_error();
+    DPV_ARG(count >= 0, "negative count");
+    if (count == 0) return DPV_OK;
+    DPV_ARG(graphs && first_free && last_free && streams && out && status, "NULL argument");
+    DPV_TRY(configure_pool());
+    std::vector<std::string> msg(count);
+    run_workers(count, threads, [&](int32_t i) {
+        out[i] = nullptr;
+        status[i] = dpv_problem_create(&graphs[i], first_free[i], last_free[i], nullptr, 0,
+                                       streams[i], &out[i]);
+        if (status[i] != DPV_OK) msg[i] = dpv_last_error();
+    });
+    return first_failure(count, status, msg);
+}
+
+int32_t dpv_lm_solve_batch(int32_t count, dpv_problem* const* probs, double* const* q,
+                           double* const* t, double* const* d, const dpv_lm_params* params,
+                           dpv_lm_report* reports, void* const* streams, int32_t threads,
+                           int32_t* status) {
+    clear_error();
+    DPV_ARG(count >= 0, "negative count");
+    if (count == 0) return DPV_OK;
+    DPV_ARG(probs && q && t && d && params && reports && streams && status, "NULL argument");
+    std::vector<std::string> msg(count);
+    run_workers(count, threads, [&](int32_t i) {
+        status[i] = dpv_lm_solve(probs[i], q[i], t[i], d[i], &params[i], &reports[i],
+                                 streams[i]);
+        if (status[i] != DPV_OK) msg[i] = dpv_last_error();
+    });
+    return first_failure(count, status, msg);
 }
 
 }  // extern "C"

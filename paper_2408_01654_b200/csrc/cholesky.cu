@@ -21,6 +21,7 @@
 //  * backward substitution L^T x = y using the diagonal-block inverses: one
 //    CTA walking the plan's nonzero tiles (sparse plans), or one cooperative
 //    persistent kernel with a grid barrier per panel (dense plans).
+#include <mutex>
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -557,6 +558,9 @@ int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, do
     DPV_ARG(ld % 8 == 0 && ld >= N + 1, "dense ld must be a multiple of 8 and > N");
     DPV_ARG(pl.N == N, "factor plan built for another size");
     const int T = pl.T, ng = pl.ng;
+    // the side streams and events are shared: one enqueuer at a time
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     DPV_TRY(setup(ng));
     Ctx& c = ctx();
     double* linv = ws;

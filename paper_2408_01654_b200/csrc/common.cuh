@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include "../../include/dpvslam_b200.h"
@@ -82,9 +83,16 @@ inline int grid_for(int64_t n, int block, int cap = 148 * 32) {
 
 int sm_count();
 
-// raise a kernel's dynamic shared-memory limit to `bytes` (once per growth)
+inline std::mutex& smem_attr_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
+// raise a kernel's dynamic shared-memory limit to `bytes` (once per growth;
+// serialised: batched solves call in from several host threads)
 template <typename K>
 int32_t ensure_smem(K kernel, size_t bytes, size_t& current) {
+    std::lock_guard<std::mutex> lk(smem_attr_mutex());
     if (bytes > current) {
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)bytes);

@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <mutex>
+
 #include "problem.cuh"
 
 namespace dpv {
@@ -1236,10 +1238,36 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     DPV_TRY(P->alloc(&P->lm_wd, NPD));
     DPV_TRY(P->alloc(&P->row_flag, NPD));
     DPV_CUDA(cudaMemsetAsync(P->status, 0, sizeof(int32_t) * 8, st));
-    DPV_CUDA(cudaMallocHost(&P->lm_host, sizeof(double) * 16));
+    P->lm_host = pinned_slot_get();
+    DPV_ARG(P->lm_host != nullptr, "pinned host allocation failed");
     DPV_CUDA(cudaStreamSynchronize(st));
     ptimer.lap("12. system arrays");
     return DPV_OK;
+}
+
+namespace {
+std::mutex g_pin_mu;
+std::vector<double*> g_pin_free;
+}  // namespace
+
+double* pinned_slot_get() {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.empty()) {
+        constexpr int kSlots = 64;
+        double* chunk = nullptr;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&chunk), sizeof(double) * 16 * kSlots,
+                          cudaHostAllocDefault) != cudaSuccess)
+            return nullptr;
+        for (int k = kSlots - 1; k >= 0; --k) g_pin_free.push_back(chunk + 16 * k);
+    }
+    double* p = g_pin_free.back();
+    g_pin_free.pop_back();
+    return p;
+}
+
+void pinned_slot_put(double* p) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(p);
 }
 
 // Lazily materialised Schur pair list (reference order: key-major, rows

@@ -40,6 +40,14 @@ int32_t spd_factor_solve(SpdPlan* pl, const int32_t* ka, const int32_t* kb, cons
                          const double* rhs, double* dp, int32_t* status, cudaStream_t st);
 }  // namespace dpv
 
+namespace dpv {
+// 16-double pinned host slots from a process-wide pool: cudaMallocHost /
+// cudaFreeHost cost milliseconds and cudaFreeHost synchronises the device,
+// which would serialise concurrently built / destroyed problems
+double* pinned_slot_get();
+void pinned_slot_put(double* p);
+}  // namespace dpv
+
 struct dpv_problem {
     // ---- sizes -------------------------------------------------------------
     int32_t F = 0;      // graph frames
@@ -188,7 +196,7 @@ struct dpv_problem {
         // returned to the device pool (release threshold raised: see
         // dpv::configure_pool), so the next problem reuses the memory
         for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
-        if (lm_host) cudaFreeHost(lm_host);
+        if (lm_host) dpv::pinned_slot_put(lm_host);
         delete plan;
         dpv::spd_plan_free(spd);
     }

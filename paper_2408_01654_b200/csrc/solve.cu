@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <mutex>
+
 #include "problem.cuh"
 
 namespace dpv {
@@ -481,6 +483,8 @@ int32_t cholesky_solve(double* a, int64_t lda, double* b, int64_t n, int32_t* st
                        double* work, cudaStream_t st) {
     // a: augmented (n+1) x lda buffer with the rhs already in row n; x -> b
     static FactorPlan dense_plan;   // every tile (the matrix pattern is unknown)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     if (dense_plan.N != n) DPV_TRY(build_factor_plan(n, nullptr, dense_plan));
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
     return dense_factor_solve(a, lda, n, status, b, work, dense_plan, st);

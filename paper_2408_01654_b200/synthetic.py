@@ -353,6 +353,12 @@ CONFIGS = {
                            look="inward", image_size=(640, 480),
                            intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0), extent=250.0),
                  loops=2000, free=lambda n: (1, n - 1)),
+    # TartanAir-shape sequences: 64 independent cfg2-style
+    # windows, sequence s uses scene seed s (make_config(..., seed=s))
+    "cfg5": dict(spec=dict(kind="circle", n_frames=40, seed=0, n_landmarks=6000, look="inward",
+                           image_size=(640, 480),
+                           intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0)),
+                 loops=0, free=lambda n: (n - 22, n - 1)),
     # KITTI shape: forward-looking square loop, 4500 frames
     "cfg4": dict(spec=dict(kind="square-loop", n_frames=4500, seed=0, n_landmarks=324000,
                            look="forward", image_size=(1226, 370),
@@ -367,18 +373,24 @@ DESCRIPTIONS = {
     "mid": "120-frame loop graph (circle, 96 patches/frame, radius 13, loop edges)",
     "cfg3": "2000-frame global loop-closure BA (circle, 96 patches/frame, radius 13, "
             "33x32 loop edges)",
+    "cfg5": "TartanAir-shape sequences (640x480), one 22-frame window step each "
+            "(96 patches/frame, radius 13), 8 per GPU as replicas",
     "cfg4": "KITTI-shape 4500-frame global BA (1226x370, forward square loop, 96 patches/frame, "
             "radius 13, 75x32 loop edges)",
 }
 
 
-def make_config(name: str, initial_targets: bool = False):
+def make_config(name: str, initial_targets: bool = False, seed: int | None = None):
     """Build a benchmark configuration: (scene, graph, free_range).
 
     Recipe: generate(96 patches, radius 13) -> bench-ba LOOP
-    edges -> fill_flow(sigma=0.3, seed=1) -> perturb_poses(0.02, seed=11)."""
+    edges -> fill_flow(sigma=0.3, seed=1) -> perturb_poses(0.02, seed=11).
+    ``seed`` overrides the scene seed (cfg5: sequence s has seed s)."""
     cfg = CONFIGS[name]
-    spec = SceneSpec(**cfg["spec"])
+    kw = dict(cfg["spec"])
+    if seed is not None:
+        kw["seed"] = int(seed)
+    spec = SceneSpec(**kw)
     scene, graph = generate(spec, 96, 13, initial_targets=initial_targets)
     if cfg["loops"]:
         add_loop_edges(graph, cfg["loops"], 96, seed=0)

@@ -1,3 +1,6 @@
-timeout 300 python -m pytest tests/test_gpu_corr.py -x -q > gpurun_out/corr_test.log 2>&1; echo corrtest=$?
-timeout 300 python tools/bench_corr.py > gpurun_out/corr.txt 2>&1; echo bc=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_corr_tma -c 1 -o gpurun_out/corr_tma python tools/bench_corr.py --reps 1 > gpurun_out/corr_ncu.log 2>&1; echo ncu=$?
+#!/bin/bash
+# batched replicas: tests + cfg5 leg
+set -x
+mkdir -p gpurun_out
+python -m pytest tests/test_gpu_batch.py tests/test_gpu_ba_parity.py tests/test_gpu_spd.py -x -q 2>&1 | tail -15
+for n in 1 8 16; do timeout 600 python tools/bench_batch.py $n 2>&1 | tail -1; done
