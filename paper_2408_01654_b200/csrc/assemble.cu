@@ -477,6 +477,202 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges(
     }
 }
 
+// Same pass in the TARGET camera's frame (default).  With B = diag(R_j, R_j)
+// the world Jacobian row is J_r = B k_r, k_r = [jp_r ; y x jp_r] where jp_r is
+// row r of Jproj and y = R_j^T x_w (rotation commutes with the cross
+// product), so per segment Sum w J^T J = B (Sum w k k^T) B^T.  k_0 has no
+// y-component (k_0[1] = 0) and k_1 no x-component (k_1[0] = 0): 15 instead of
+// 21 Gram FMAs per residual row.  The point chain uses Rrel = R_j^T R_i and
+// u = R_j^T (t_i - t_j) (x_t = Rrel x_c + u; J_depth = -jp_r . Rrel x_c / d,
+// since t_i - x_w = -R_i x_c).  The per-edge e_pd and the per-segment sums
+// are rotated back to world coordinates, so the outputs keep their meaning
+// (ba.py:355-366); values agree with the world-frame pass to rounding.
+template <int Z>
+__device__ __forceinline__ void gram_row(const double (&k)[6], double wv, double rr, double jd,
+                                         double (&H)[21], double (&G)[6], double (&ep)[6],
+                                         double& cdd, double& gd, double& fobj) {
+    double wk[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) wk[a] = (a == Z) ? 0.0 : k[a] * wv;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+        if (a == Z) continue;
+#pragma unroll
+        for (int b = a; b < 6; ++b) {
+            if (b == Z) continue;
+            H[utri(a, b)] += wk[a] * k[b];
+        }
+        G[a] += wk[a] * rr;
+        ep[a] += wk[a] * jd;
+    }
+    const double wjd = jd * wv;
+    cdd += wjd * jd;
+    gd += wjd * rr;
+    fobj += wv * rr * rr;
+}
+
+template <int U, int MINB, bool PF>
+__global__ void __launch_bounds__(128, MINB) k_assemble_edges_loc(
+    int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
+    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
+    const double* __restrict__ a_w, const double* __restrict__ r_ray,
+    const double* __restrict__ Rall, const double* __restrict__ tall,
+    const double* __restrict__ d, double fx, double fy, double cx, double cy,
+    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g,
+    double* __restrict__ seg_obj) {
+    constexpr int M = 9;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // per warp: [0,24) raw frames (R_i t_i R_j t_j), [24,33) Rrel, [33,36) u,
+    // [36,39) c = R_j^T t_j, [40,76) local 6x6 Gram, [76,82) local gradient
+    __shared__ double sfr[4][82];
+    double* fr = sfr[threadIdx.x >> 5];
+    const double* Ri = fr;
+    const double* ti = fr + 9;
+    const double* Rj = fr + 12;
+    const double* tj = fr + 21;
+    const double* Rr = fr + 24;
+    const double* uu = fr + 33;
+    const double* cc = fr + 36;
+    double* Hs = fr + 40;
+    double* Gs = fr + 76;
+    for (int64_t s = warp; s < S; s += nwarps) {
+        const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
+        __syncwarp();
+        if (lane < 12) {
+            const int32_t f = seg_src[s];
+            fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
+        } else if (lane < 24) {
+            const int32_t f = seg_dst[s];
+            fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
+        }
+        __syncwarp();
+        if (lane < 9) {               // Rrel[a][b] = sum_m R_j[m][a] R_i[m][b]
+            const int a = lane / 3, b = lane % 3;
+            fr[24 + lane] = Rj[a] * Ri[b] + Rj[3 + a] * Ri[3 + b] + Rj[6 + a] * Ri[6 + b];
+        } else if (lane < 12) {       // u = R_j^T (t_i - t_j)
+            const int a = lane - 9;
+            fr[24 + lane] = Rj[a] * (ti[0] - tj[0]) + Rj[3 + a] * (ti[1] - tj[1]) +
+                            Rj[6 + a] * (ti[2] - tj[2]);
+        } else if (lane < 15) {       // c = R_j^T t_j
+            const int a = lane - 12;
+            fr[24 + lane] = Rj[a] * tj[0] + Rj[3 + a] * tj[1] + Rj[6 + a] * tj[2];
+        }
+        __syncwarp();
+        double H[21], G[6];
+        double fobj = 0.0;
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) G[k] = 0.0;
+        int32_t rn1 = (PF && e0 + lane + 32 < e1) ? a_row[e0 + lane + 32] : 0;
+        for (int32_t e = e0 + lane; e < e1; e += 32) {
+            if (PF) {
+                const int32_t en = e + 32;
+                int32_t rn2 = 0;
+                if (en < e1) {
+#pragma unroll
+                    for (int c = 0; c < 2 * M; ++c) {
+                        prefetch_l1(a_tgt + (int64_t)c * E + en);
+                        prefetch_l1(r_ray + (int64_t)c * P + rn1);
+                    }
+                    prefetch_l1(a_w + en);
+                    prefetch_l1(a_w + E + en);
+                    prefetch_l1(d + rn1);
+                    if (en + 32 < e1) rn2 = a_row[en + 32];
+                }
+                rn1 = rn2;
+            }
+            const int32_t row = a_row[e];
+            const double id = __drcp_rn(__ldg(d + row));
+            const double w0 = a_w[e], w1 = a_w[E + e];
+            double ep[6] = {0, 0, 0, 0, 0, 0};
+            double cdd = 0.0, gd = 0.0;
+#pragma unroll U
+            for (int c = 0; c < M; ++c) {
+                const double xc0 = __ldg(r_ray + (int64_t)(2 * c) * P + row) * id;
+                const double xc1 = __ldg(r_ray + (int64_t)(2 * c + 1) * P + row) * id;
+                double xr[3], xt[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    xr[a] = Rr[3 * a] * xc0 + Rr[3 * a + 1] * xc1 + Rr[3 * a + 2] * id;
+                    xt[a] = xr[a] + uu[a];
+                }
+                const bool valid = xt[2] > kDepthEps;
+                const double iz = __drcp_rn(valid ? xt[2] : 1.0);
+                const double t0 = xt[0] * iz, t1 = xt[1] * iz;
+                const double p0 = fx * iz, p1 = fy * iz;
+                const double q0 = -p0 * t0, q1 = -p1 * t1;
+                const double y0 = xt[0] + cc[0], y1 = xt[1] + cc[1], y2 = xt[2] + cc[2];
+                const double k0[6] = {p0, 0.0, q0, y1 * q0, y2 * p0 - y0 * q0, -y1 * p0};
+                const double k1[6] = {0.0, p1, q1, y1 * q1 - y2 * p1, -y0 * q1, y0 * p1};
+                const double jd0 = -(p0 * xr[0] + q0 * xr[2]) * id;
+                const double jd1 = -(p1 * xr[1] + q1 * xr[2]) * id;
+                const double r0 = (fx * t0 + cx) - a_tgt[(int64_t)(2 * c) * E + e];
+                const double r1 = (fy * t1 + cy) - a_tgt[(int64_t)(2 * c + 1) * E + e];
+                gram_row<1>(k0, valid ? w0 : 0.0, r0, jd0, H, G, ep, cdd, gd, fobj);
+                gram_row<0>(k1, valid ? w1 : 0.0, r1, jd1, H, G, ep, cdd, gd, fobj);
+            }
+            // e_pd back to world coordinates: B ep
+            double ew[6];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    ew[3 * h + a] = Rj[3 * a] * ep[3 * h] + Rj[3 * a + 1] * ep[3 * h + 1] +
+                                    Rj[3 * a + 2] * ep[3 * h + 2];
+            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
+            et[0] = make_double2(ew[0], ew[1]);
+            et[1] = make_double2(ew[2], ew[3]);
+            et[2] = make_double2(ew[4], ew[5]);
+            et[3] = make_double2(cdd, gd);
+        }
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
+        fobj = warp_sum(fobj);
+        if (seg_obj && lane == 0) seg_obj[s] = fobj;
+        // local sums -> shared (full symmetric 6x6), then B H B^T and B G
+        for (int idx = lane; idx < 36; idx += 32) {
+            const int a = idx / 6, b = idx % 6;
+            const int t = a <= b ? utri(a, b) : utri(b, a);
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 21; ++q) v = (q == t) ? H[q] : v;
+            Hs[idx] = v;
+        }
+        if (lane < 6) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
+            Gs[lane] = v;
+        }
+        __syncwarp();
+        if (lane < 21) {
+            int a = 0;
+            while (a < 5 && utri(a + 1, a + 1) <= lane) ++a;
+            const int b = a + (lane - utri(a, a));
+            const int al = a % 3, ab = (a / 3) * 3, bl = b % 3, bb = (b / 3) * 3;
+            double v = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < 3; ++pp) {
+                const double* hr = Hs + (ab + pp) * 6 + bb;
+                const double inner = hr[0] * Rj[3 * bl] + hr[1] * Rj[3 * bl + 1] +
+                                     hr[2] * Rj[3 * bl + 2];
+                v += Rj[3 * al + pp] * inner;
+            }
+            seg_h[s * 21 + lane] = v;
+        } else if (lane < 27) {
+            const int a = lane - 21, al = a % 3, ab = (a / 3) * 3;
+            seg_g[s * 6 + a] = Rj[3 * al] * Gs[ab] + Rj[3 * al + 1] * Gs[ab + 1] +
+                               Rj[3 * al + 2] * Gs[ab + 2];
+        }
+    }
+}
+
 // depth side (ba.py:370-373): per-row sums over the row's edges
 __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32_t* row_pos,
                        const double* e_terms, double* depth_diag, double* rhs_depth,
@@ -878,13 +1074,23 @@ int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, co
         p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,        \
         p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
         p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr)
+#define DPV_ASML(U, B, PF)                                                                     \
+    k_assemble_edges_loc<U, B, PF><<<blocks, 32 * warps_per_block, 0, st>>>(                   \
+        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,      \
+        p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],            \
+        p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr)
         switch (variant) {
             case 1: DPV_ASM(3, 3, false); break;
             case 2: DPV_ASM(1, 3, true); break;
             case 3: DPV_ASM(3, 2, true); break;
-            default: DPV_ASM(3, 3, true); break;
+            case 4: DPV_ASM(3, 3, true); break;       // world-frame pass
+            case 5: DPV_ASML(3, 4, true); break;
+            case 6: DPV_ASML(1, 3, true); break;
+            case 7: DPV_ASML(3, 3, true); break;
+            default: DPV_ASML(9, 3, true); break;
         }
 #undef DPV_ASM
+#undef DPV_ASML
         DPV_CHECK_LAUNCH();
     }
     if (obj) {
