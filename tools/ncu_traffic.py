@@ -13,7 +13,9 @@ import sys
 NAMES = {"k_assemble_edges": "assemble_edges", "k_objective_seg": "objective",
          "k_objective": "objective", "k_corr_mma": "corr", "k_corr": "corr",
          "k_key_blocks": "key_blocks", "k_spd_factor": "spd_factor",
-         "k_incidences": "incidences", "k_coords_sel": "coords"}
+         "k_incidences": "incidences", "k_coords_sel": "coords",
+         "k_assemble_edges_loc": "assemble_edges", "k_corr_tma": "corr", "k_rows": "rows",
+         "k_var_rhs": "var_rhs", "k_spd_schur": "spd_schur"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
