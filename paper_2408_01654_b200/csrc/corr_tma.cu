@@ -96,6 +96,14 @@ __device__ __forceinline__ uint32_t ld_sw(const unsigned char* base, int row, in
                                               (ch & 7) * 2);
 }
 
+// four 8x8 b16 matrices from shared memory; lane l addresses row l % 8 of
+// matrix l / 8 (16 contiguous bytes = one swizzle chunk)
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], unsigned addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+
 __device__ __forceinline__ void mma_bf16_t(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -232,6 +240,24 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
     }
     // ---------------- consumers (4 warps) ----------------
     const int g = lane >> 2, t4 = lane & 3;
+    // ldmatrix lane roles (128B swizzle: chunk' = chunk ^ (row % 8), rows of
+    // a tile start 1024-aligned so row % 8 = lane % 8 for every matrix):
+    // A (16 patch rows x 2 chunks): row l%8 + 8*((l/8)&1), chunk +(l/16)
+    // B (8 tap rows x 4 chunks = two k-steps): row nt*8 + l%8, chunk +(l/8)
+    const int l7 = lane & 7;
+    const unsigned offA = (unsigned)((l7 + 8 * ((lane >> 3) & 1)) * 128);
+    const unsigned mA = (unsigned)(((lane >> 4) ^ l7) << 4);
+    const unsigned offB = (unsigned)((warp * 8 + l7) * 128);
+    const unsigned mB = (unsigned)(((lane >> 3) ^ l7) << 4);
+    // blend slots of this thread (x = tid + 128 i < 441), fixed for all items
+    int slot_c[4], slot_off[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int x = tid + kConsumers * i;
+        const int c = x / (O * O), ab = x % (O * O);
+        slot_c[i] = x < kCellsT * O * O ? c : -1;
+        slot_off[i] = c * kTapsPad + (ab / O) * kWin + ab % O;
+    }
     for (int64_t u = 0; u < n_my; ++u) {
         const int s = (int)(u % kStages);
         mbar_wait(&full[s], (unsigned)((u / kStages) & 1));
@@ -245,22 +271,20 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
             for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
-                const unsigned char* Wh = st + h * kHalfBytes;
-                const unsigned char* Gh = Gs + h * kGHalfBytes;
+                const unsigned wb = smem_u32(st + h * kHalfBytes) + offB;
+                const unsigned gb = smem_u32(Gs + h * kGHalfBytes) + offA;
 #pragma unroll
-                for (int k0 = 0; k0 < 64; k0 += 16) {
-                    uint32_t a[4];
-                    a[0] = ld_sw(Gh, g, k0 + 2 * t4);
-                    a[1] = ld_sw(Gh, g + 8, k0 + 2 * t4);
-                    a[2] = ld_sw(Gh, g, k0 + 2 * t4 + 8);
-                    a[3] = ld_sw(Gh, g + 8, k0 + 2 * t4 + 8);
+                for (int kc = 0; kc < 8; kc += 4) {     // 16-byte chunk = 8 channels
+                    uint32_t a0[4], a1[4];
+                    ldsm_x4(a0, gb + ((unsigned)(kc << 4) ^ mA));
+                    ldsm_x4(a1, gb + ((unsigned)((kc + 2) << 4) ^ mA));
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const int nt = warp + 4 * q;
-                        if (nt < 13) {
-                            const int n = nt * 8 + g;
-                            mma_bf16_t(acc[q], a, ld_sw(Wh, n, k0 + 2 * t4),
-                                       ld_sw(Wh, n, k0 + 2 * t4 + 8));
+                        if (warp + 4 * q < 13) {
+                            uint32_t b[4];
+                            ldsm_x4(b, wb + q * 4096 + ((unsigned)(kc << 4) ^ mB));
+                            mma_bf16_t(acc[q], a0, b[0], b[1]);
+                            mma_bf16_t(acc[q], a1, b[2], b[3]);
                         }
                     }
                 }
@@ -279,12 +303,14 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
                 }
             }
             bar_consumers();
-            for (int x = tid; x < kCellsT * O * O; x += kConsumers) {
-                const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
-                const CellMeta cm = M->cell[c];
-                const float* sp = S + c * kTapsPad + (cm.oy + a) * kWin + cm.ox + bb;
-                o[x] = (1.f - cm.fy) * ((1.f - cm.fx) * sp[0] + cm.fx * sp[1]) +
-                       cm.fy * ((1.f - cm.fx) * sp[kWin] + cm.fx * sp[kWin + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (slot_c[i] < 0) continue;
+                const CellMeta cm = M->cell[slot_c[i]];
+                const float* sp = S + slot_off[i] + cm.oy * kWin + cm.ox;
+                o[tid + kConsumers * i] =
+                    (1.f - cm.fy) * ((1.f - cm.fx) * sp[0] + cm.fx * sp[1]) +
+                    cm.fy * ((1.f - cm.fx) * sp[kWin] + cm.fx * sp[kWin + 1]);
             }
         } else {
             // wide or non-finite window: per-cell integer-tap dots from global memory
