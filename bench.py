@@ -246,8 +246,9 @@ class Stepper:
         P = L.ptr
         from paper_2408_01654_b200 import corr
         torch = self.torch
+        L.check(lib.dpv_assemble(self.h, P(q), P(t), P(d), s), "assemble")
         # K2 pixels of the correlation edges -> K1, on a side stream: the
-        # correlation is independent of this BA step and overlaps it
+        # correlation is independent of this BA step and overlaps the solve
         self.ev_fork.record()
         side = self.side if self.overlap else torch.cuda.current_stream()
         with torch.cuda.stream(side):
@@ -257,7 +258,6 @@ class Stepper:
                     "coords")
             corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
             self.ev_join.record()
-        L.check(lib.dpv_assemble(self.h, P(q), P(t), P(d), s), "assemble")
         if w["sharded"]:
             w["prob"].allreduce_system()      # NCCL: reduced pose system
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
