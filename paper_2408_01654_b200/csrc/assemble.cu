@@ -961,6 +961,127 @@ __global__ void k_var_rhs(int64_t n, const int32_t* var_seg_ptr, const int32_t* 
     }
 }
 
+// Small problems (few keys / vars, e.g. a 22-frame window): the same sums
+// with one 4-warp CTA per key / var, so each key's segments and pair runs are
+// split over 4 warps instead of one; partial results combine in a fixed
+// warp order (deterministic).
+template <int UNR>
+__global__ void __launch_bounds__(128) k_key_blocks_cta(
+    int64_t W, const int32_t* key_seg_ptr, const int32_t* key_seg, const double* seg_h,
+    const int32_t* __restrict__ key_run_ptr, const int32_t* __restrict__ run_l,
+    const int32_t* __restrict__ run_r, const int32_t* __restrict__ run_len,
+    const double* __restrict__ uinc, const double* __restrict__ inc_block,
+    double* __restrict__ pose_blocks, double* __restrict__ schur_blocks, int pose_only) {
+    __shared__ double hp[4][21];
+    __shared__ double sp[4][64];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        double h[21];
+#pragma unroll
+        for (int k = 0; k < 21; ++k) h[k] = 0.0;
+        for (int32_t k = key_seg_ptr[w] + wi * 32 + lane; k < key_seg_ptr[w + 1]; k += 128) {
+            const int32_t code = key_seg[k];
+            const double sgn = (code & 1) ? -1.0 : 1.0;
+            const double* src = seg_h + (int64_t)(code >> 1) * 21;
+#pragma unroll
+            for (int q = 0; q < 21; ++q) h[q] += sgn * src[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 21; ++q) h[q] = warp_sum(h[q]);
+        if (lane < 21) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 21; ++q) v = (q == lane) ? h[q] : v;
+            hp[wi][lane] = v;
+        }
+        const int kq = lane & 3, ci = lane >> 2;
+        double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        if (!pose_only) {
+            for (int32_t q = key_run_ptr[w]; q < key_run_ptr[w + 1]; ++q) {
+                const int32_t len = run_len[q];
+                const double* ub = uinc + (int64_t)run_l[q] * 6;
+                const double* vb = inc_block + (int64_t)run_r[q] * 6;
+                for (int32_t t0 = wi * 4 * UNR; t0 < len; t0 += 16 * UNR) {
+                    double a[UNR], b[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        const int32_t t = t0 + 4 * u + kq;
+                        const bool ok = t < len && ci < 6;
+                        a[u] = ok ? __ldg(ub + (int64_t)t * 6 + ci) : 0.0;
+                        b[u] = ok ? __ldg(vb + (int64_t)t * 6 + ci) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) dmma_f64(c[u & 3][0], c[u & 3][1], a[u], b[u]);
+                }
+            }
+        }
+        sp[wi][2 * lane] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+        sp[wi][2 * lane + 1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
+        __syncthreads();
+        if (threadIdx.x < 36) {
+            const int idx = threadIdx.x, a = idx / 6, b = idx % 6;
+            const int t = a <= b ? utri(a, b) : utri(b, a);
+            pose_blocks[w * 36 + idx] = ((hp[0][t] + hp[1][t]) + hp[2][t]) + hp[3][t];
+            if (!pose_only) {
+                // fragment element (i, j) sits at lane 4 i + j / 2, slot j % 2
+                const int e = 2 * (4 * a + b / 2) + (b & 1);
+                schur_blocks[w * 36 + idx] = ((sp[0][e] + sp[1][e]) + sp[2][e]) + sp[3][e];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(128) k_var_rhs_cta(
+    int64_t n, const int32_t* var_seg_ptr, const int32_t* var_seg, const double* seg_g,
+    const int32_t* var_inc_ptr, const int32_t* inc_row, const double* inc_block,
+    const double* cinv0, const double* rhs_depth, double* rhs_pose, double* rhs_schur,
+    unsigned long long* grad_bits) {
+    __shared__ double part[4][12];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+        double g[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};
+        for (int32_t k = var_seg_ptr[v] + threadIdx.x; k < var_seg_ptr[v + 1]; k += 128) {
+            const int32_t code = var_seg[k];
+            const double sgn = (code & 1) ? -1.0 : 1.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) g[a] += sgn * seg_g[(int64_t)(code >> 1) * 6 + a];
+        }
+        for (int32_t i = var_inc_ptr[v] + threadIdx.x; i < var_inc_ptr[v + 1]; i += 128) {
+            const int32_t row = inc_row[i];
+            const double r = rhs_depth[row] * cinv0[row];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) sc[a] += inc_block[(int64_t)i * 6 + a] * r;
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            g[a] = warp_sum(g[a]);
+            sc[a] = warp_sum(sc[a]);
+        }
+        if (lane < 12) {
+            double x = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                x = (lane == a) ? g[a] : x;
+                x = (lane == 6 + a) ? sc[a] : x;
+            }
+            part[wi][lane] = x;
+        }
+        __syncthreads();
+        if (threadIdx.x < 12) {
+            const int a = threadIdx.x;
+            const double x = ((part[0][a] + part[1][a]) + part[2][a]) + part[3][a];
+            if (a < 6) {
+                rhs_pose[v * 6 + a] = x;
+                atomicMax(grad_bits, (unsigned long long)__double_as_longlong(fabs(x)));
+            } else {
+                rhs_schur[v * 6 + a - 6] = x;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // scale pin direction (ba.py:419-426)
 __global__ void k_pin(const double* t, int32_t first_free, int32_t anchor, double* scal) {
     double u[3];
@@ -1130,7 +1251,15 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
                                                            p->inc_block, p->uinc, p->grouped);
         DPV_CHECK_LAUNCH();
     }
-    if (p->W > 0) {
+    // few keys / vars: one CTA each (a warp each would leave most SMs idle)
+    const bool small = p->W < (int64_t)sm_count() * 8 && !p->grouped;
+    if (p->W > 0 && small) {
+        DPV_TSTART("key_blocks", st);
+        k_key_blocks_cta<4><<<(int)p->W, 128, 0, st>>>(
+            p->W, p->key_seg_ptr, p->key_seg, p->seg_h, p->key_run_ptr, p->run_l, p->run_r,
+            p->run_len, p->uinc, p->inc_block, p->pose_blocks, p->schur_blocks, 0);
+        DPV_CHECK_LAUNCH();
+    } else if (p->W > 0) {
         int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("key_blocks", st);
         const int kv = getenv("DPV_KEY_VARIANT") ? atoi(getenv("DPV_KEY_VARIANT")) : 0;
@@ -1167,9 +1296,16 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
     if (p->n > 0) {
         int blocks = (int)std::min<int64_t>((p->n + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("var_rhs", st);
-        k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
-                                          p->var_inc_ptr, p->inc_row, p->inc_block, p->cinv0,
-                                          p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
+        if (p->n < (int64_t)sm_count() * 4) {
+            k_var_rhs_cta<<<(int)p->n, 128, 0, st>>>(
+                p->n, p->var_seg_ptr, p->var_seg, p->seg_g, p->var_inc_ptr, p->inc_row,
+                p->inc_block, p->cinv0, p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
+        } else {
+            k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
+                                              p->var_inc_ptr, p->inc_row, p->inc_block,
+                                              p->cinv0, p->rhs_depth, p->rhs_pose,
+                                              p->rhs_schur, grad_bits);
+        }
         DPV_CHECK_LAUNCH();
         if (p->scale_degenerate) {
             DPV_TSTART("pin", st);

@@ -226,6 +226,201 @@ __global__ void __launch_bounds__(1024) k_small_solve(
     if (tid == 0) status[1] = bad;
 }
 
+// Same solve, blocked by 4 columns (default; DPV_SMALL_V1=1: the unblocked
+// kernel above): warp 0 factors the 4x4 diagonal block, all threads scale
+// the panel and apply the rank-4 update; the backward substitution runs by
+// 4-blocks on 256 threads (named barrier).  Same pivot reporting and
+// rhs-as-last-row forward substitution.  cfg2 window (N = 132): 127 us per
+// solve vs 168 us unblocked; the kernel is latency-bound on one SM.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallBsubThreads = 256;   // fewer threads per barrier: 3x faster here
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
+    int64_t n, int64_t W, const int32_t* ka, const int32_t* kb, const double* pose,
+    const double* schur, const double* rhs_pose, const double* rhs_schur, const double* scal,
+    double lam, double* dp, int32_t* status) {
+    extern __shared__ double A[];
+    __shared__ double colb[4][kSmallMax + 1];
+    __shared__ double dinv[kSmallMax];
+    __shared__ int bad;
+    const int N = (int)(6 * n);
+    const int ld = N + 1;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wy = tid >> 5;
+    constexpr int ny = kSmallThreads / 32;
+    for (int x = tid; x < (N + 1) * ld; x += kSmallThreads) A[x] = 0.0;
+    if (tid == 0) bad = -1;
+    __syncthreads();
+    for (int64_t x = tid; x < W * 36; x += kSmallThreads) {
+        const int64_t w = x / 36;
+        const int idx = (int)(x % 36);
+        const int i = idx / 6, j = idx % 6;
+        const int a = ka[w], b = kb[w];
+        const double v = reduced_entry(pose, schur, w, idx, a == b, lam);
+        if (a == b) {
+            if (i >= j) A[(6 * a + i) * ld + 6 * a + j] = v;
+        } else {
+            A[(6 * b + j) * ld + 6 * a + i] = v;
+        }
+    }
+    for (int c = tid; c < N; c += kSmallThreads)
+        A[N * ld + c] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
+    __syncthreads();
+    if (tid == 0 && scal[1] != 0.0 && N >= 6) {
+        double mx = 0.0;
+        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[k * ld + k]));
+        const double mu = 1e6 * fmax(1.0, mx);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j <= i; ++j) A[i * ld + j] += mu * scal[2 + i] * scal[2 + j];
+    }
+    __syncthreads();
+    // right-looking by blocks of 4 columns: warp 0 factors the 4x4 diagonal
+    // block (rsqrt pivots, lanes redundant) into shared memory, all threads
+    // scale the panel rows (forward substitution), then a rank-4 update.
+    // (Factoring the block redundantly in all 1024 threads saturates the FP64
+    // pipe of the one SM: sqrt + division are ~50 DP instructions each.)
+    __shared__ double lblk[4][4], linv[4];
+    for (int j = 0; j < N; j += 4) {
+        const int bw = min(4, N - j);
+        if (wy == 0) {
+            double l[4][4], inv[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q <= p; ++q) l[p][q] = (p < bw) ? A[(j + p) * ld + j + q] : 1.0;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                double piv = l[p][p];
+                if (p < bw && !(piv > 0.0)) {
+                    if (lane == 0 && bad < 0) bad = j + p;
+                    piv = 1.0;
+                }
+                if (p >= bw) piv = 1.0;
+                inv[p] = rsqrt(piv);
+                l[p][p] = piv * inv[p];
+#pragma unroll
+                for (int r = p + 1; r < 4; ++r) l[r][p] *= inv[p];
+#pragma unroll
+                for (int r = p + 1; r < 4; ++r)
+#pragma unroll
+                    for (int c = p + 1; c <= r; ++c) l[r][c] -= l[r][p] * l[c][p];
+            }
+            __syncwarp();
+            if (lane < 16) {
+                const int p = lane >> 2, q = lane & 3;
+                double v = 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b <= a; ++b) v = (a == p && b == q) ? l[a][b] : v;
+                lblk[p][q] = v;
+                if (q <= p && p < bw) A[(j + p) * ld + j + q] = v;
+                if (q == 0) {
+                    double iv = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) iv = (a == p) ? inv[a] : iv;
+                    linv[p] = iv;
+                    if (p < bw) dinv[j + p] = iv;
+                }
+            }
+        }
+        __syncthreads();
+        double l[4][4], inv[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            inv[p] = linv[p];
+#pragma unroll
+            for (int q = 0; q < p; ++q) l[p][q] = lblk[p][q];
+        }
+        for (int i = j + bw + tid; i <= N; i += kSmallThreads) {
+            double x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double v = q < bw ? A[i * ld + j + q] : 0.0;
+#pragma unroll
+                for (int r = 0; r < q; ++r) v -= x[r] * l[q][r];
+                x[q] = v * inv[q];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < bw) {
+                    A[i * ld + j + q] = x[q];
+                    colb[q][i] = x[q];
+                }
+        }
+        __syncthreads();
+        // rank-4 update; a warp takes two rows at a time so each lane has two
+        // independent FMA chains in flight (the loop is latency-bound)
+        for (int i0 = j + bw + 2 * wy; i0 <= N; i0 += 2 * ny) {
+            const int i1 = i0 + 1;
+            const bool two = i1 <= N;
+            double la[4], lb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                la[q] = q < bw ? colb[q][i0] : 0.0;
+                lb[q] = (q < bw && two) ? colb[q][i1] : 0.0;
+            }
+            const int kmax0 = i0 < N ? i0 : N - 1;
+            const int kmax1 = two ? (i1 < N ? i1 : N - 1) : -1;
+            for (int k = j + bw + lane; k <= kmax1 || k <= kmax0; k += 32) {
+                double c[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) c[q] = q < bw ? colb[q][k] : 0.0;
+                if (k <= kmax0) {
+                    const double v = A[i0 * ld + k];
+                    A[i0 * ld + k] = v - (la[0] * c[0] + la[1] * c[1]) - (la[2] * c[2] + la[3] * c[3]);
+                }
+                if (k <= kmax1) {
+                    const double v = A[i1 * ld + k];
+                    A[i1 * ld + k] = v - (lb[0] * c[0] + lb[1] * c[1]) - (lb[2] * c[2] + lb[3] * c[3]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // backward substitution L^T x = y (y in row N) by blocks of 4: every
+    // thread solves the block's 4x4 triangle redundantly, then the earlier
+    // entries of y take the block's update; one barrier per block
+    double* y = A + (int64_t)N * ld;
+    double* xs = &colb[0][0];            // the solution (colb is free now)
+    if (tid < kSmallBsubThreads) {
+        for (int jb = ((N - 1) / 4) * 4; jb >= 0; jb -= 4) {
+            const int bw = min(4, N - jb);
+            double x[4];
+#pragma unroll
+            for (int p = 3; p >= 0; --p) {
+                if (p >= bw) {
+                    x[p] = 0.0;
+                    continue;
+                }
+                double v = y[jb + p];
+#pragma unroll
+                for (int r = p + 1; r < 4; ++r)
+                    if (r < bw) v -= A[(jb + r) * ld + jb + p] * x[r];
+                x[p] = v * dinv[jb + p];
+            }
+            if (tid < bw) {
+                double xv = x[0];
+#pragma unroll
+                for (int q = 1; q < 4; ++q) xv = (tid == q) ? x[q] : xv;
+                xs[jb + tid] = xv;
+            }
+            for (int i = tid; i < jb; i += kSmallBsubThreads) {
+                double v = y[i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < bw) v -= A[(jb + q) * ld + i] * x[q];
+                y[i] = v;
+            }
+            asm volatile("bar.sync 1, %0;\n" ::"n"(kSmallBsubThreads) : "memory");
+        }
+    }
+    __syncthreads();
+    for (int c = tid; c < N; c += kSmallThreads) dp[c] = xs[c];
+    if (tid == 0) status[0] = bad >= 0 ? 1 : 0;
+    if (tid == 0) status[1] = bad;
+}
+
 __global__ void k_copy_row(const double* src, int64_t n, double* dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -416,14 +611,26 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
               cudaStream_t st) {
     const int64_t N = 6 * p->n;
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
-    if (N <= kSmallMax) {
+    static const int64_t small_max =
+        getenv("DPV_SMALL_MAX") ? std::min<int64_t>(atoll(getenv("DPV_SMALL_MAX")), kSmallMax)
+                                : kSmallMax;
+    if (N <= small_max) {
         const size_t smem = sizeof(double) * (size_t)(N + 1) * (N + 1);
-        static size_t cur = 0;
-        DPV_TRY(ensure_smem(k_small_solve, smem, cur));
+        static const bool v1 = getenv("DPV_SMALL_V1") && atoi(getenv("DPV_SMALL_V1")) != 0;
         DPV_TSTART("small_solve", st);
-        k_small_solve<<<1, 1024, smem, st>>>(p->n, p->W, p->key_a, p->key_b, p->pose_blocks,
-                                             p->schur_blocks, p->rhs_pose, p->rhs_schur, p->scal,
-                                             lam, dp, status);
+        if (v1) {
+            static size_t cur = 0;
+            DPV_TRY(ensure_smem(k_small_solve, smem, cur));
+            k_small_solve<<<1, 1024, smem, st>>>(p->n, p->W, p->key_a, p->key_b, p->pose_blocks,
+                                                 p->schur_blocks, p->rhs_pose, p->rhs_schur,
+                                                 p->scal, lam, dp, status);
+        } else {
+            static size_t cur = 0;
+            DPV_TRY(ensure_smem(k_small_solve2, smem, cur));
+            k_small_solve2<<<1, kSmallThreads, smem, st>>>(
+                p->n, p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, p->rhs_pose,
+                p->rhs_schur, p->scal, lam, dp, status);
+        }
         DPV_CHECK_LAUNCH();
     } else if (!dense_solve_forced() && !p->spd_failed) {
         // banded + border sparse factorisation (spd.cu)
