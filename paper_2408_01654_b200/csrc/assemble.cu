@@ -673,6 +673,243 @@ __global__ void __launch_bounds__(128, MINB) k_assemble_edges_loc(
     }
 }
 
+// The local-frame edge pass with its inputs staged through shared memory:
+// per warp a double-buffered ring of 32-edge items (one lane per edge).
+// While item i computes, item i+1's targets, weights, rays and depth are in
+// flight as 8-byte cp.async copies (its rows were loaded one item earlier),
+// so the FP64 chain no longer waits on global-load latency.  Segments are cut
+// into items of <= 32 edges; the Gram sums run across a segment's items and
+// are reduced / rotated to world coordinates after its last item.
+constexpr int kStgVals = 39;                  // 18 targets, 18 rays, 2 weights, depth
+constexpr int kStgDoubles = kStgVals * 32;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
+struct EdgeItem {
+    int64_t s;        // segment (>= S: none)
+    int32_t e0, e1;   // this item's edge range
+    int32_t se1;      // segment end
+};
+
+template <int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
+    int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
+    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
+    const double* __restrict__ a_w, const double* __restrict__ r_ray,
+    const double* __restrict__ Rall, const double* __restrict__ tall,
+    const double* __restrict__ d, double fx, double fy, double cx, double cy,
+    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g,
+    double* __restrict__ seg_obj) {
+    extern __shared__ double stg_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double* ring = stg_raw + (int64_t)wib * 2 * kStgDoubles;
+    __shared__ double sfr[NW][82];
+    double* fr = sfr[wib];
+    const double* Ri = fr;
+    const double* ti = fr + 9;
+    const double* Rj = fr + 12;
+    const double* tj = fr + 21;
+    const double* Rr = fr + 24;
+    const double* uu = fr + 33;
+    const double* cc = fr + 36;
+    double* Hs = fr + 40;
+    double* Gs = fr + 76;
+
+    auto first_item = [&](int64_t s) {
+        EdgeItem it;
+        it.s = s;
+        if (s < S) {
+            it.e0 = seg_ptr[s];
+            it.se1 = seg_ptr[s + 1];
+            it.e1 = min(it.e0 + 32, it.se1);
+        } else {
+            it.e0 = it.e1 = it.se1 = 0;
+        }
+        return it;
+    };
+    auto next_item = [&](const EdgeItem& it) {
+        if (it.s < S && it.e1 < it.se1) {
+            EdgeItem n = it;
+            n.e0 = it.e1;
+            n.e1 = min(n.e0 + 32, it.se1);
+            return n;
+        }
+        return first_item(it.s + nwarps);
+    };
+    auto row_of = [&](const EdgeItem& it) -> int32_t {
+        const int32_t e = it.e0 + lane;
+        return (it.s < S && e < it.e1) ? __ldg(a_row + e) : 0;
+    };
+    auto issue = [&](const EdgeItem& it, int32_t row, double* b) {
+        const int32_t e = it.e0 + lane;
+        if (it.s < S && e < it.e1) {
+#pragma unroll
+            for (int c = 0; c < 18; ++c) cp_async8(b + c * 32 + lane, a_tgt + (int64_t)c * E + e);
+#pragma unroll
+            for (int c = 0; c < 18; ++c)
+                cp_async8(b + (18 + c) * 32 + lane, r_ray + (int64_t)c * P + row);
+            cp_async8(b + 36 * 32 + lane, a_w + e);
+            cp_async8(b + 37 * 32 + lane, a_w + E + e);
+            cp_async8(b + 38 * 32 + lane, d + row);
+        }
+        cp_async_commit();
+    };
+
+    EdgeItem cur = first_item(warp);
+    EdgeItem nx = next_item(cur);
+    int32_t row_cur = row_of(cur);
+    int32_t row_nx = row_of(nx);
+    issue(cur, row_cur, ring);
+    double H[21], G[6];
+    double fobj = 0.0;
+    int buf = 0;
+    while (cur.s < S) {
+        // stage the next item, load the rows of the one after
+        const EdgeItem nx2 = next_item(nx);
+        const int32_t row_nx2 = row_of(nx2);
+        issue(nx, row_nx, ring + (buf ^ 1) * kStgDoubles);
+        const bool seg_first = cur.e0 == seg_ptr[cur.s];
+        if (seg_first) {
+            __syncwarp();
+            if (lane < 12) {
+                const int32_t f = seg_src[cur.s];
+                fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
+            } else if (lane < 24) {
+                const int32_t f = seg_dst[cur.s];
+                fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12)
+                                     : __ldg(tall + 3 * f + lane - 21);
+            }
+            __syncwarp();
+            if (lane < 9) {
+                const int a = lane / 3, b = lane % 3;
+                fr[24 + lane] = Rj[a] * Ri[b] + Rj[3 + a] * Ri[3 + b] + Rj[6 + a] * Ri[6 + b];
+            } else if (lane < 12) {
+                const int a = lane - 9;
+                fr[24 + lane] = Rj[a] * (ti[0] - tj[0]) + Rj[3 + a] * (ti[1] - tj[1]) +
+                                Rj[6 + a] * (ti[2] - tj[2]);
+            } else if (lane < 15) {
+                const int a = lane - 12;
+                fr[24 + lane] = Rj[a] * tj[0] + Rj[3 + a] * tj[1] + Rj[6 + a] * tj[2];
+            }
+#pragma unroll
+            for (int k = 0; k < 21; ++k) H[k] = 0.0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) G[k] = 0.0;
+            fobj = 0.0;
+        }
+        cp_async_wait1();
+        __syncwarp();
+        const double* b = ring + buf * kStgDoubles;
+        const int32_t e = cur.e0 + lane;
+        if (e < cur.e1) {
+            const double id = __drcp_rn(b[38 * 32 + lane]);
+            const double w0 = b[36 * 32 + lane], w1 = b[37 * 32 + lane];
+            double ep[6] = {0, 0, 0, 0, 0, 0};
+            double cdd = 0.0, gd = 0.0;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                const double xc0 = b[(18 + 2 * c) * 32 + lane] * id;
+                const double xc1 = b[(19 + 2 * c) * 32 + lane] * id;
+                double xr[3], xt[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    xr[a] = Rr[3 * a] * xc0 + Rr[3 * a + 1] * xc1 + Rr[3 * a + 2] * id;
+                    xt[a] = xr[a] + uu[a];
+                }
+                const bool valid = xt[2] > kDepthEps;
+                const double iz = __drcp_rn(valid ? xt[2] : 1.0);
+                const double t0 = xt[0] * iz, t1 = xt[1] * iz;
+                const double p0 = fx * iz, p1 = fy * iz;
+                const double q0 = -p0 * t0, q1 = -p1 * t1;
+                const double y0 = xt[0] + cc[0], y1 = xt[1] + cc[1], y2 = xt[2] + cc[2];
+                const double k0[6] = {p0, 0.0, q0, y1 * q0, y2 * p0 - y0 * q0, -y1 * p0};
+                const double k1[6] = {0.0, p1, q1, y1 * q1 - y2 * p1, -y0 * q1, y0 * p1};
+                const double jd0 = -(p0 * xr[0] + q0 * xr[2]) * id;
+                const double jd1 = -(p1 * xr[1] + q1 * xr[2]) * id;
+                const double r0 = (fx * t0 + cx) - b[(2 * c) * 32 + lane];
+                const double r1 = (fy * t1 + cy) - b[(2 * c + 1) * 32 + lane];
+                gram_row<1>(k0, valid ? w0 : 0.0, r0, jd0, H, G, ep, cdd, gd, fobj);
+                gram_row<0>(k1, valid ? w1 : 0.0, r1, jd1, H, G, ep, cdd, gd, fobj);
+            }
+            double ew[6];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    ew[3 * h + a] = Rj[3 * a] * ep[3 * h] + Rj[3 * a + 1] * ep[3 * h + 1] +
+                                    Rj[3 * a + 2] * ep[3 * h + 2];
+            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
+            et[0] = make_double2(ew[0], ew[1]);
+            et[1] = make_double2(ew[2], ew[3]);
+            et[2] = make_double2(ew[4], ew[5]);
+            et[3] = make_double2(cdd, gd);
+        }
+        if (cur.e1 == cur.se1) {          // segment done: reduce, rotate, write
+            const int64_t sg = cur.s;
+#pragma unroll
+            for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
+            fobj = warp_sum(fobj);
+            if (seg_obj && lane == 0) seg_obj[sg] = fobj;
+            for (int idx = lane; idx < 36; idx += 32) {
+                const int a = idx / 6, bb = idx % 6;
+                const int t = a <= bb ? utri(a, bb) : utri(bb, a);
+                double v = 0.0;
+#pragma unroll
+                for (int q = 0; q < 21; ++q) v = (q == t) ? H[q] : v;
+                Hs[idx] = v;
+            }
+            if (lane < 6) {
+                double v = 0.0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
+                Gs[lane] = v;
+            }
+            __syncwarp();
+            if (lane < 21) {
+                int a = 0;
+                while (a < 5 && utri(a + 1, a + 1) <= lane) ++a;
+                const int bb = a + (lane - utri(a, a));
+                const int al = a % 3, ab = (a / 3) * 3, bl = bb % 3, bo = (bb / 3) * 3;
+                double v = 0.0;
+#pragma unroll
+                for (int pp = 0; pp < 3; ++pp) {
+                    const double* hr = Hs + (ab + pp) * 6 + bo;
+                    const double inner = hr[0] * Rj[3 * bl] + hr[1] * Rj[3 * bl + 1] +
+                                         hr[2] * Rj[3 * bl + 2];
+                    v += Rj[3 * al + pp] * inner;
+                }
+                seg_h[sg * 21 + lane] = v;
+            } else if (lane < 27) {
+                const int a = lane - 21, al = a % 3, ab = (a / 3) * 3;
+                seg_g[sg * 6 + a] = Rj[3 * al] * Gs[ab] + Rj[3 * al + 1] * Gs[ab + 1] +
+                                    Rj[3 * al + 2] * Gs[ab + 2];
+            }
+        }
+        __syncwarp();                     // buffer `buf` and the frames are free
+        cur = nx;
+        nx = nx2;
+        row_nx = row_nx2;
+        buf ^= 1;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // depth side (ba.py:370-373): per-row sums over the row's edges
 __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32_t* row_pos,
                        const double* e_terms, double* depth_diag, double* rhs_depth,
@@ -1208,7 +1445,32 @@ int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, co
             case 5: DPV_ASML(3, 4, true); break;
             case 6: DPV_ASML(1, 3, true); break;
             case 7: DPV_ASML(3, 3, true); break;
-            default: DPV_ASML(9, 3, true); break;
+            case 8: DPV_ASML(9, 3, true); break;
+            default: {
+                // persistent: every warp walks many segments so the staging
+                // pipeline stays full (MINB resident blocks per SM)
+                auto launch = [&](auto kern, int nw, int minb) -> int32_t {
+                    const size_t smem = sizeof(double) * 2 * kStgDoubles * nw;
+                    static size_t cur[4] = {0, 0, 0, 0};
+                    DPV_TRY(ensure_smem(kern, smem, cur[nw - 1]));
+                    const int pblocks = (int)std::min<int64_t>((p->S + nw - 1) / nw,
+                                                               (int64_t)sm_count() * minb);
+                    kern<<<pblocks, 32 * nw, smem, st>>>(
+                        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row,
+                        p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1],
+                        p->intr[2], p->intr[3], p->e_terms, p->seg_h, p->seg_g,
+                        obj ? p->seg_obj : nullptr);
+                    return DPV_OK;
+                };
+                // 4 warps x 2 blocks (198 registers, 8 warps per SM): 0.64 ms at
+                // cfg3; 3x3 / 2x5 / 1x10 cap the registers at 168 and run
+                // 0.83-0.86 ms
+                if (variant == 10) DPV_TRY(launch(k_assemble_edges_stg<3, 3>, 3, 3));
+                else if (variant == 11) DPV_TRY(launch(k_assemble_edges_stg<1, 10>, 1, 10));
+                else if (variant == 12) DPV_TRY(launch(k_assemble_edges_stg<2, 5>, 2, 5));
+                else DPV_TRY(launch(k_assemble_edges_stg<4, 2>, 4, 2));
+                break;
+            }
         }
 #undef DPV_ASM
 #undef DPV_ASML
