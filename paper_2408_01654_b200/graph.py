@@ -333,7 +333,7 @@ class PatchGraph:
         self._kf.extend([bool(is_keyframe)])
         self._feat.extend([True])
         k = len(depths)
-        self._grid.extend(np.asarray(grids, dtype=float).reshape(k, -1, 2))
+        self._grid.extend(np.asarray(grids, dtype=float).reshape(k, self.patch_size ** 2, 2))
         self._depth.extend(depths)
         self._lm.extend(np.full(k, -1) if landmarks is None else landmarks)
         self._poff.append(self._poff[-1] + k)

@@ -409,6 +409,28 @@ def case_synth(with_cfg3):
     print(f"wrote {path}")
 
 
+def case_fixture():
+    """Text fixture written by the reference's own writer (graph.py:268-296):
+    a small perturbed scene plus loop edges, one frame without dense features
+    and landmark extras; the SoA state beside it pins the parser."""
+    from patchslam.graph import write_graph
+    spec = SceneSpec(kind="circle", n_frames=6, seed=3, n_landmarks=600, look="inward")
+    scene, graph = generate(spec, patches_per_frame=8, odometry_radius=2)
+    graph.add_edges([(5, k, 0) for k in range(3)], kind=LOOP)
+    fill_flow(graph, scene, OracleConfig(outlier_fraction=0.2), seed=2)
+    perturb_poses(graph, 0.03, seed=4)
+    graph.frames[2].has_dense_features = False
+    out = {}
+    put_graph(out, graph)
+    out["g_timestamp"] = np.array([f.timestamp for f in graph.frames])
+    out["g_keyframe"] = np.array([f.is_keyframe for f in graph.frames])
+    out["g_features"] = np.array([f.has_dense_features for f in graph.frames])
+    extras = [f"landmark {i} {x!r} {y!r} {z!r}"
+              for i, (x, y, z) in enumerate(np.asarray(scene.landmarks)[:3].tolist())]
+    write_graph(graph, os.path.join(HERE, "graph_fixture.txt"), extras)
+    save("fixture", out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true")
@@ -416,7 +438,7 @@ if __name__ == "__main__":
     args = ap.parse_args()
     cases = {"small": case_small, "window": case_window, "loops": case_loops,
              "edges": case_edges, "reproject": case_reproject, "cholesky": case_cholesky,
-             "detect": case_detect,
+             "detect": case_detect, "fixture": case_fixture,
              "synth": lambda: case_synth(args.with_cfg3)}
     for name, fn in cases.items():
         if args.only and name not in args.only.split(","):
