@@ -577,6 +577,7 @@ def run_ours(args):
     # global loop-closure BA (loop.close: new BAProblem + solve(8 iters, 1e-9))
     glob = None
     window = None
+    window1 = None
     batch = None
     if not args.no_global and world == 1:
         glob = run_global(work, args, torch)
@@ -584,6 +585,10 @@ def run_ours(args):
             window = run_window(args, torch)
         except Exception as exc:     # reported, not fatal for the headline
             window = {"error": repr(exc)}
+        try:
+            window1 = run_window(args, torch, config="cfg1")
+        except Exception as exc:
+            window1 = {"error": repr(exc)}
         try:
             batch = None if args.no_batch else run_batch(args, torch, n_seq=args.batch_seqs)
         except Exception as exc:
@@ -631,6 +636,7 @@ def run_ours(args):
         "index_build_ms": work["build_ms"],
         "global_ba": glob,
         "window_step": window,
+        "window_step_cfg1": window1,
         "batch_replicas": batch,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -834,13 +840,13 @@ def run_e2e_solve(work, args, torch, steps=6):
                     "depths (wall clock; next upload double-buffered)"}
 
 
-def run_window(args, torch, reps=5):
+def run_window(args, torch, reps=5, config="cfg2"):
     """Local odometry window at EuRoC shape (BASELINE configs[1], cfg2): per
     frame-step a new BAProblem over the 22-frame window, the correlation of
     every window edge (2 levels, bf16) and ba.solve(2 LM iterations, tol 1e-12)
     as pipeline.py:389-396 runs it.  Launch/latency-bound (55k edges)."""
     from paper_2408_01654_b200 import ba, corr, synthetic
-    scene, graph, free = synthetic.make_config("cfg2")
+    scene, graph, free = synthetic.make_config(config)
     soa0 = {k: np.array(v) for k, v in graph.soa().items()}
     w, h = scene.spec.image_size
     C = args.channels
@@ -883,8 +889,11 @@ def run_window(args, torch, reps=5):
             times.append((time.perf_counter() - t0) * 1e3)
         del prob
     ms = float(np.median(times))
-    return {"config": "cfg2: EuRoC 752x480, 22-frame window, 96 patches/frame, corr (2 levels) "
-                      "+ BAProblem + solve(2 LM iterations)",
+    desc = {"cfg1": "cfg1: 16-frame local window (640x480), 96 patches/frame, corr (2 levels) "
+                    "+ BAProblem + solve(2 LM iterations)",
+            "cfg2": "cfg2: EuRoC 752x480, 22-frame window, 96 patches/frame, corr (2 levels) "
+                    "+ BAProblem + solve(2 LM iterations)"}
+    return {"config": desc.get(config, config),
             "E": E, "ms": ms, "value": 2 * E / (ms * 1e-3), "unit": "patch-edges/s (x2 LM iters)",
             "iterations": rep.iterations, "final_objective": rep.final_objective,
             "includes": "index build, correlation, native LM, write-back (wall clock, synced)"}
