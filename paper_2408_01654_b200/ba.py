@@ -661,8 +661,6 @@ def solve_batch(problems, max_iterations: int = 50, tolerance: float = 1e-9,
     SingularSystem instance where ``solve`` would have raised (that problem's
     graph is then left unwritten, as in ``solve``).  max_iterations, tolerance
     and backend_threshold may be scalars or one value per problem."""
-    torch = _torch()
-    build_batch(problems, threads)
     n = len(problems)
     if n == 0:
         return []
@@ -676,6 +674,8 @@ def solve_batch(problems, max_iterations: int = 50, tolerance: float = 1e-9,
     for c in chosen:
         if c not in _BACKENDS:
             raise KeyError(c)
+    torch = _torch()
+    build_batch(problems, threads)
     active = [p.active_patch_count() for p in problems]
     states = [p.device_state() for p in problems]
     streams = [getattr(p, "_stream", None) or torch.cuda.Stream() for p in problems]
