@@ -352,43 +352,82 @@ __global__ void k_sub_one(int64_t n, int32_t* a) {
 // Schur pair runs without materialising the pairs.  Pair (il, ir) of a depth
 // row continues a run iff (il-1, ir-1) is a pair of the same key: both
 // incidences belong to the same vars and share a row.  MODE 0 counts the run
-// heads per row, MODE 1 writes them in pair order (deterministic).
+// heads per row, MODE 1 writes them in pair order (deterministic).  The
+// row's incidences (index, var, and the row of the previous incidence of the
+// same var, or -1) are staged in shared memory once, then the pairs
+// (l, r >= l) are tested l-major with lanes over r: no triangular index
+// decode and no per-pair gathers.  Rows with more than kPhMax incidences
+// take a per-pair path.
+constexpr int kPhMax = 128;
+
 template <int MODE>
-__global__ void k_pair_heads(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
-                             const int32_t* inc_var, const int32_t* inc_row, int64_t nfree,
-                             int32_t* hcount, const int64_t* hoff, uint64_t* hkey, int32_t* hl,
-                             int32_t* hr) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) k_pair_heads_staged(
+    int64_t P, const int32_t* rinc_ptr, const int32_t* rinc, const int32_t* inc_var,
+    const int32_t* inc_row, int64_t nfree, int32_t* hcount, const int64_t* hoff, uint64_t* hkey,
+    int32_t* hl, int32_t* hr) {
+    __shared__ int32_t s_il[8][kPhMax], s_var[8][kPhMax], s_prev[8][kPhMax];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int32_t* il_s = s_il[wib];
+    int32_t* var_s = s_var[wib];
+    int32_t* prev_s = s_prev[wib];
     for (int64_t r = warp; r < P; r += nwarps) {
         const int32_t s = rinc_ptr[r];
         const int32_t m = rinc_ptr[r + 1] - s;
-        const int64_t tot = (int64_t)m * (m + 1) / 2;
         int64_t base = MODE ? hoff[r] : 0;
         int32_t cnt = 0;
-        for (int64_t k0 = 0; k0 < tot; k0 += 32) {
-            const int64_t k = k0 + lane;
-            bool head = false;
-            int32_t il = 0, ir = 0;
-            if (k < tot) {
-                int32_t l = 0;
-                int64_t rowlen = m, acc = 0;
-                while (acc + rowlen <= k) { acc += rowlen; --rowlen; ++l; }
-                const int32_t rr = l + (int32_t)(k - acc);
-                il = rinc[s + l];
-                ir = rinc[s + rr];
-                head = !(il > 0 && ir > 0 && inc_var[il - 1] == inc_var[il] &&
-                         inc_var[ir - 1] == inc_var[ir] && inc_row[il - 1] == inc_row[ir - 1]);
+        if (m > kPhMax) {      // per-pair path
+            const int64_t tot = (int64_t)m * (m + 1) / 2;
+            for (int64_t k0 = 0; k0 < tot; k0 += 32) {
+                const int64_t k = k0 + lane;
+                bool head = false;
+                int32_t il = 0, ir = 0;
+                if (k < tot) {
+                    int32_t l = 0;
+                    int64_t rowlen = m, acc = 0;
+                    while (acc + rowlen <= k) { acc += rowlen; --rowlen; ++l; }
+                    const int32_t rr = l + (int32_t)(k - acc);
+                    il = rinc[s + l];
+                    ir = rinc[s + rr];
+                    head = !(il > 0 && ir > 0 && inc_var[il - 1] == inc_var[il] &&
+                             inc_var[ir - 1] == inc_var[ir] && inc_row[il - 1] == inc_row[ir - 1]);
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, head);
+                if (MODE == 1 && head) {
+                    const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
+                    hkey[pos] = (uint64_t)inc_var[il] * (uint64_t)nfree + (uint64_t)inc_var[ir];
+                    hl[pos] = il;
+                    hr[pos] = ir;
+                }
+                cnt += __popc(bal);
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, head);
-            if (MODE == 1 && head) {
-                const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
-                hkey[pos] = (uint64_t)inc_var[il] * (uint64_t)nfree + (uint64_t)inc_var[ir];
-                hl[pos] = il;
-                hr[pos] = ir;
+        } else {
+            __syncwarp();
+            for (int j = lane; j < m; j += 32) {
+                const int32_t il = rinc[s + j];
+                const int32_t v = inc_var[il];
+                il_s[j] = il;
+                var_s[j] = v;
+                prev_s[j] = (il > 0 && inc_var[il - 1] == v) ? inc_row[il - 1] : -1;
             }
-            cnt += __popc(bal);
+            __syncwarp();
+            for (int l = 0; l < m; ++l) {
+                const int32_t pl = prev_s[l];
+                for (int r0 = l; r0 < m; r0 += 32) {
+                    const int rr = r0 + lane;
+                    const bool act = rr < m;
+                    const bool head = act && !(pl >= 0 && prev_s[rr] == pl);
+                    const unsigned bal = __ballot_sync(0xffffffffu, head);
+                    if (MODE == 1 && head) {
+                        const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
+                        hkey[pos] = (uint64_t)var_s[l] * (uint64_t)nfree + (uint64_t)var_s[rr];
+                        hl[pos] = il_s[l];
+                        hr[pos] = il_s[rr];
+                    }
+                    cnt += __popc(bal);
+                }
+            }
         }
         if (MODE == 0 && lane == 0) hcount[r] = cnt;
     }
@@ -908,7 +947,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_TRY(sc.get(&hcount64, NPD + 1));
         DPV_TRY(sc.get(&hoff, NPD + 1));
         if (NPD > 0) {
-            k_pair_heads<0><<<grid_for(NPD * 32, B), B, 0, st>>>(
+            k_pair_heads_staged<0><<<grid_for(NPD * 32, B), B, 0, st>>>(
                 NPD, P->rinc_ptr, P->rinc, P->inc_var, P->inc_row, P->n, hcount, nullptr, nullptr,
                 nullptr, nullptr);
             DPV_CHECK_LAUNCH();
@@ -931,7 +970,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         DPV_TRY(sc.get(&hid, nr));
         DPV_TRY(sc.get(&hid_s, nr));
         if (NPD > 0) {
-            k_pair_heads<1><<<grid_for(NPD * 32, B), B, 0, st>>>(
+            k_pair_heads_staged<1><<<grid_for(NPD * 32, B), B, 0, st>>>(
                 NPD, P->rinc_ptr, P->rinc, P->inc_var, P->inc_row, P->n, nullptr, hoff, hk, hl,
                 hr);
             DPV_CHECK_LAUNCH();
