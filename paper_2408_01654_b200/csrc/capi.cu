@@ -355,6 +355,7 @@ int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_
         delete p;
         return s;
     }
+    spd_plan_prefetch(p);
     *out = p;
     return DPV_OK;
 }

@@ -2,6 +2,7 @@
 // assembled system arrays (ba.py:272-440).  One handle per BAProblem.
 #pragma once
 
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -33,6 +34,7 @@ struct SpdPlan;
 int32_t spd_plan_build(const int32_t* ka, const int32_t* kb, int64_t W, int64_t n, SpdPlan** out,
                        cudaStream_t st);
 void spd_plan_free(SpdPlan* p);
+void spd_plan_set_stream(SpdPlan* p, cudaStream_t st);
 int64_t spd_plan_bytes(const SpdPlan* p);
 void spd_plan_describe(const SpdPlan* p, int64_t* v);
 double spd_plan_flops(const SpdPlan* p);
@@ -163,6 +165,11 @@ struct dpv_problem {
     int32_t* perm_pos = nullptr;   // (n) pose var -> permuted position in the dense solve
     dpv::SpdPlan* spd = nullptr;   // sparse band+border solver plan (lazily built)
     int32_t spd_failed = 0;        // plan impossible -> tile-plan factorisation
+    // the plan is host work (~1 ms at cfg3): built on a host thread started
+    // by the index build, joined by the first sparse solve
+    std::thread plan_thread;
+    dpv::SpdPlan* spd_pending = nullptr;
+    int32_t plan_status = 0;
     double* sblk = nullptr;        // (W, 36) S(lambda) blocks for the sparse solver
     int32_t* status = nullptr;     // (4) device flags
 
@@ -193,6 +200,8 @@ struct dpv_problem {
         return DPV_OK;
     }
     ~dpv_problem() {
+        if (plan_thread.joinable()) plan_thread.join();
+        dpv::spd_plan_free(spd_pending);
         // returned to the device pool (release threshold raised: see
         // dpv::configure_pool), so the next problem reuses the memory
         for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
@@ -238,6 +247,7 @@ int32_t coords_sel(dpv_problem* p, const double* q, const double* t, const doubl
                    cudaStream_t st);
 int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
                        cudaStream_t st);
+void spd_plan_prefetch(dpv_problem* p);
 int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,
               cudaStream_t st);
 int32_t apply_step(dpv_problem* p, const double* q, const double* t, const double* d,

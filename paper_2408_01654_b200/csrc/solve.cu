@@ -607,6 +607,47 @@ int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, 
     return DPV_OK;
 }
 
+// Start the sparse-solver plan on a host thread right after the index build
+// (the union keys are final), so its ~1 ms of host work overlaps the first
+// edge pass and assembly on the device.  Same plan, same failure fallback
+// as building it inside the first solve.  DPV_SPD_SYNC_PLAN=1: build in solve.
+void spd_plan_prefetch(dpv_problem* p) {
+    static const bool sync_plan = getenv("DPV_SPD_SYNC_PLAN") &&
+                                  atoi(getenv("DPV_SPD_SYNC_PLAN")) != 0;
+    if (sync_plan || 6 * p->n <= kSmallMax || p->W == 0 || dense_solve_forced() ||
+        p->plan_thread.joinable() || p->spd)
+        return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    p->plan_thread = std::thread([p, dev]() {
+        cudaSetDevice(dev);
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+            p->plan_status = DPV_CUDA_ERROR;
+            return;
+        }
+        std::vector<int32_t> ka(p->W), kb(p->W);
+        int32_t rc = DPV_OK;
+        if (cudaMemcpyAsync(ka.data(), p->key_a, sizeof(int32_t) * p->W, cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaMemcpyAsync(kb.data(), p->key_b, sizeof(int32_t) * p->W, cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            rc = DPV_CUDA_ERROR;
+        dpv::SpdPlan* pl = nullptr;
+        if (rc == DPV_OK) rc = spd_plan_build(ka.data(), kb.data(), p->W, p->n, &pl, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) rc = DPV_CUDA_ERROR;
+        if (rc == DPV_OK) {
+            spd_plan_set_stream(pl, p->alloc_stream);   // freed with the problem
+            p->spd_pending = pl;
+        } else {
+            spd_plan_free(pl);
+        }
+        p->plan_status = rc;
+        cudaStreamDestroy(s);
+    });
+}
+
 int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,
               cudaStream_t st) {
     const int64_t N = 6 * p->n;
@@ -634,6 +675,17 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
         DPV_CHECK_LAUNCH();
     } else if (!dense_solve_forced() && !p->spd_failed) {
         // banded + border sparse factorisation (spd.cu)
+        if (!p->spd && p->plan_thread.joinable()) {
+            p->plan_thread.join();           // built beside the first edge pass
+            p->spd = p->spd_pending;
+            p->spd_pending = nullptr;
+            if (p->plan_status != DPV_OK || !p->spd) {
+                p->spd = nullptr;
+                p->spd_failed = 1;
+                return solve(p, lam, dp, dd, status, st);
+            }
+            DPV_TRY(p->alloc(&p->sblk, p->W * 36));
+        }
         if (!p->spd) {
             std::vector<int32_t> ka(p->W), kb(p->W);
             DPV_CUDA(cudaMemcpyAsync(ka.data(), p->key_a, sizeof(int32_t) * p->W,
