@@ -920,9 +920,20 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
          r += (int64_t)gridDim.x * blockDim.x) {
         double c = 0.0, g = 0.0;
-        for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
-            const int32_t e = row_pos[k];
-            const double2 cg = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)e * 8 + 6));
+        const int32_t k1 = row_ptr[r + 1];
+        int32_t k = row_ptr[r];
+        for (; k + 1 < k1; k += 2) {       // two gathers in flight, same order
+            const int32_t ea = __ldg(row_pos + k), eb = __ldg(row_pos + k + 1);
+            const double2 ca = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)ea * 8 + 6));
+            const double2 cb = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)eb * 8 + 6));
+            c += ca.x;
+            g += ca.y;
+            c += cb.x;
+            g += cb.y;
+        }
+        if (k < k1) {
+            const double2 cg = __ldg(reinterpret_cast<const double2*>(
+                e_terms + (int64_t)__ldg(row_pos + k) * 8 + 6));
             c += cg.x;
             g += cg.y;
         }
@@ -945,6 +956,65 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
             atomicMax(grad_bits + 7, gb);   // depth-only part (sharded BA)
         }
         if (inact) atomicAdd(n_inactive, inact);
+    }
+}
+
+// same sums, two contributions per step (both gathers in flight before the
+// adds; same summation order) and 16-byte stores
+__global__ void __launch_bounds__(256) k_incidences2(int64_t I, const int32_t* __restrict__ inc_ptr,
+                                                     const int32_t* __restrict__ inc_con,
+                                                     const int32_t* __restrict__ inc_row,
+                                                     const double* __restrict__ e_terms,
+                                                     const double* __restrict__ cinv0,
+                                                     double* __restrict__ inc_block,
+                                                     double* __restrict__ uinc, int sym) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        const int32_t k0 = inc_ptr[i], k1 = inc_ptr[i + 1];
+        const double c0 = __ldg(cinv0 + inc_row[i]);
+        int32_t k = k0;
+        for (; k + 1 < k1; k += 2) {
+            const int32_t ca = __ldg(inc_con + k), cb = __ldg(inc_con + k + 1);
+            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 8);
+            const double2* eb = reinterpret_cast<const double2*>(e_terms + (int64_t)(cb >> 1) * 8);
+            double2 va[3], vb[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                va[a] = __ldg(ea + a);
+                vb[a] = __ldg(eb + a);
+            }
+            const double sa = (ca & 1) ? -1.0 : 1.0, sb = (cb & 1) ? -1.0 : 1.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                acc[2 * a] += sa * va[a].x;
+                acc[2 * a + 1] += sa * va[a].y;
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                acc[2 * a] += sb * vb[a].x;
+                acc[2 * a + 1] += sb * vb[a].y;
+            }
+        }
+        if (k < k1) {
+            const int32_t ca = __ldg(inc_con + k);
+            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 8);
+            const double sa = (ca & 1) ? -1.0 : 1.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double2 v = __ldg(ea + a);
+                acc[2 * a] += sa * v.x;
+                acc[2 * a + 1] += sa * v.y;
+            }
+        }
+        const double c = sym ? sqrt(c0) : c0;
+        double2* ib = reinterpret_cast<double2*>(inc_block + i * 6);
+        double2* ub = reinterpret_cast<double2*>(uinc + i * 6);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ib[a] = make_double2(acc[2 * a], acc[2 * a + 1]);
+            ub[a] = make_double2(acc[2 * a] * c, acc[2 * a + 1] * c);
+        }
     }
 }
 
@@ -1508,9 +1578,15 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
     }
     if (p->I > 0) {
         DPV_TSTART("incidences", st);
-        k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
-                                                           p->inc_row, p->e_terms, p->cinv0,
-                                                           p->inc_block, p->uinc, p->grouped);
+        const int iv = getenv("DPV_INC_VARIANT") ? atoi(getenv("DPV_INC_VARIANT")) : 0;
+        if (iv == 1)
+            k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
+                                                               p->inc_row, p->e_terms, p->cinv0,
+                                                               p->inc_block, p->uinc, p->grouped);
+        else
+            k_incidences2<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->inc_ptr, p->inc_con,
+                                                                p->inc_row, p->e_terms, p->cinv0,
+                                                                p->inc_block, p->uinc, p->grouped);
         DPV_CHECK_LAUNCH();
     }
     // few keys / vars: one CTA each (a warp each would leave most SMs idle)

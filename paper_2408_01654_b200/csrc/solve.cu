@@ -438,7 +438,32 @@ __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int3
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
          r += (int64_t)gridDim.x * blockDim.x) {
         double acc = 0.0;
-        for (int32_t k = rinc_ptr[r]; k < rinc_ptr[r + 1]; ++k) {
+        const int32_t k1 = rinc_ptr[r + 1];
+        int32_t k = rinc_ptr[r];
+        for (; k + 1 < k1; k += 2) {       // two incidences in flight, same order
+            const int32_t ia = __ldg(rinc + k), ib = __ldg(rinc + k + 1);
+            const double* ba = inc_block + (int64_t)ia * 6;
+            const double* bb = inc_block + (int64_t)ib * 6;
+            const double* xa = dp + (int64_t)__ldg(inc_var + ia) * 6;
+            const double* xb = dp + (int64_t)__ldg(inc_var + ib) * 6;
+            double va[6], vb[6], wa[6], wb[6];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                va[a] = __ldg(ba + a);
+                vb[a] = __ldg(bb + a);
+                wa[a] = __ldg(xa + a);
+                wb[a] = __ldg(xb + a);
+            }
+            double sa = 0.0, sb = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                sa += va[a] * wa[a];
+                sb += vb[a] * wb[a];
+            }
+            acc += sa;
+            acc += sb;
+        }
+        if (k < k1) {
             const int32_t i = rinc[k];
             const double* blk = inc_block + (int64_t)i * 6;
             const double* x = dp + (int64_t)inc_var[i] * 6;

@@ -60,7 +60,10 @@ def main():
         tm = _lib.timing_collect()
         _lib.timing_enable(False)
         ae = tm.get("assemble_edges", (0, 1))
-        print(f"assemble variant {v}: chain {ms:.3f} ms, k_assemble_edges {ae[0] / ae[1]:.3f} ms")
+        inc = tm.get("incidences", (0, 1))
+        print(f"assemble variant {v}: chain {ms:.3f} ms, k_assemble_edges {ae[0] / ae[1]:.3f} ms, "
+              f"incidences {inc[0] / inc[1]:.3f} ms (DPV_INC_VARIANT="
+              f"{os.environ.get('DPV_INC_VARIANT', '0')})")
     for v in a.key_variants.split(","):
         os.environ["DPV_KEY_VARIANT"] = v
         _lib.timing_enable(True)
