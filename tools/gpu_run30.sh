@@ -5,4 +5,4 @@ python bench.py --steps 10 --no-e2e --no-cpu --no-batch --json-out gpurun_out/b3
 python -c "
 import json;d=json.load(open('gpurun_out/b30.json'));g=d['global_ba']
 print('step',d['ms_per_step'],'value',d['value'],'global',g['ms'])
-for k in ('rows','incidences','key_blocks','back_substitute','assemble_edges','spd_factor'): print(k, round(d['kernels'][k]['ms_per_step'],4))"
+for k in ("rows","incidences","key_blocks","var_rhs","back_substitute","assemble_edges","spd_factor"): print(k, round(d['kernels'][k]['ms_per_step'],4))"
