@@ -15,7 +15,8 @@ NAMES = {"k_assemble_edges": "assemble_edges", "k_objective_seg": "objective",
          "k_key_blocks": "key_blocks", "k_spd_factor": "spd_factor",
          "k_incidences": "incidences", "k_coords_sel": "coords",
          "k_assemble_edges_loc": "assemble_edges", "k_corr_tma": "corr", "k_rows": "rows",
-         "k_var_rhs": "var_rhs", "k_spd_schur": "spd_schur", "k_incidences2": "incidences"}
+         "k_var_rhs": "var_rhs", "k_spd_schur": "spd_schur", "k_incidences2": "incidences",
+         "k_assemble_edges_stg": "assemble_edges"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
