@@ -333,6 +333,10 @@ def time_steps(fn, k, torch):
     for _ in range(k):
         fn()
     b.record()
+    # wait with the GIL released so the clock sampler thread keeps polling
+    # while the device runs (graph replays return immediately)
+    while not b.query():
+        time.sleep(0.0002)
     torch.cuda.synchronize()
     return a.elapsed_time(b)
 
