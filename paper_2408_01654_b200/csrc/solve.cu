@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(1024) k_small_solve(
 // kernel above): warp 0 factors the 4x4 diagonal block, all threads scale
 // the panel and apply the rank-4 update; the backward substitution runs by
 // 4-blocks on 256 threads (named barrier).  Same pivot reporting and
-// rhs-as-last-row forward substitution.  cfg2 window (N = 132): 127 us per
+// rhs-as-last-row forward substitution.  cfg2 window (N = 132): 107 us per
 // solve vs 168 us unblocked; the kernel is latency-bound on one SM.
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallBsubThreads = 256;   // fewer threads per barrier: 3x faster here
@@ -362,7 +362,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
             }
             const int kmax0 = i0 < N ? i0 : N - 1;
             const int kmax1 = two ? (i1 < N ? i1 : N - 1) : -1;
-            for (int k = j + bw + lane; k <= kmax1 || k <= kmax0; k += 32) {
+            // N <= kSmallMax: at most 6 column chunks of 32, fully unrolled so
+            // every chunk's loads are in flight together
+            constexpr int kChunks = (kSmallMax + 31) / 32;
+#pragma unroll
+            for (int it = 0; it < kChunks; ++it) {
+                const int k = j + bw + lane + 32 * it;
+                if (k > kmax0 && k > kmax1) continue;
                 double c[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) c[q] = q < bw ? colb[q][k] : 0.0;
