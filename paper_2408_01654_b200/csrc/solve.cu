@@ -230,7 +230,9 @@ __global__ void __launch_bounds__(1024) k_small_solve(
 // kernel above): warp 0 factors the 4x4 diagonal block, all threads scale
 // the panel and apply the rank-4 update; the backward substitution runs by
 // 4-blocks on 256 threads (named barrier).  Same pivot reporting and
-// rhs-as-last-row forward substitution.  cfg2 window (N = 132): 107 us per
+// rhs-as-last-row forward substitution.  Warp 0 factors the NEXT diagonal
+// block (its rank-4 update first) while the other warps update the rest, so
+// the pivot chain is off the barrier path.  cfg2 window (N = 132): 89 us per
 // solve vs 168 us unblocked; the kernel is latency-bound on one SM.
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallBsubThreads = 256;   // fewer threads per barrier: 3x faster here
@@ -279,58 +281,62 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
     // scale the panel rows (forward substitution), then a rank-4 update.
     // (Factoring the block redundantly in all 1024 threads saturates the FP64
     // pipe of the one SM: sqrt + division are ~50 DP instructions each.)
-    __shared__ double lblk[4][4], linv[4];
-    for (int j = 0; j < N; j += 4) {
+    __shared__ double lblk[2][4][4], linv[2][4];
+    // warp 0: factor diagonal block at column j (buffer b) -> lblk/linv, A, dinv
+    auto factor_diag = [&](int j, int b) {
         const int bw = min(4, N - j);
-        if (wy == 0) {
-            double l[4][4], inv[4];
+        double l[4][4], inv[4];
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
+        for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int q = 0; q <= p; ++q) l[p][q] = (p < bw) ? A[(j + p) * ld + j + q] : 1.0;
+            for (int q = 0; q <= p; ++q) l[p][q] = (p < bw) ? A[(j + p) * ld + j + q] : 1.0;
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                double piv = l[p][p];
-                if (p < bw && !(piv > 0.0)) {
-                    if (lane == 0 && bad < 0) bad = j + p;
-                    piv = 1.0;
-                }
-                if (p >= bw) piv = 1.0;
-                inv[p] = rsqrt(piv);
-                l[p][p] = piv * inv[p];
-#pragma unroll
-                for (int r = p + 1; r < 4; ++r) l[r][p] *= inv[p];
-#pragma unroll
-                for (int r = p + 1; r < 4; ++r)
-#pragma unroll
-                    for (int c = p + 1; c <= r; ++c) l[r][c] -= l[r][p] * l[c][p];
+        for (int p = 0; p < 4; ++p) {
+            double piv = l[p][p];
+            if (p < bw && !(piv > 0.0)) {
+                if (lane == 0 && bad < 0) bad = j + p;
+                piv = 1.0;
             }
-            __syncwarp();
-            if (lane < 16) {
-                const int p = lane >> 2, q = lane & 3;
-                double v = 0.0;
+            if (p >= bw) piv = 1.0;
+            inv[p] = rsqrt(piv);
+            l[p][p] = piv * inv[p];
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+            for (int r = p + 1; r < 4; ++r) l[r][p] *= inv[p];
 #pragma unroll
-                    for (int b = 0; b <= a; ++b) v = (a == p && b == q) ? l[a][b] : v;
-                lblk[p][q] = v;
-                if (q <= p && p < bw) A[(j + p) * ld + j + q] = v;
-                if (q == 0) {
-                    double iv = 0.0;
+            for (int r = p + 1; r < 4; ++r)
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) iv = (a == p) ? inv[a] : iv;
-                    linv[p] = iv;
-                    if (p < bw) dinv[j + p] = iv;
-                }
+                for (int c = p + 1; c <= r; ++c) l[r][c] -= l[r][p] * l[c][p];
+        }
+        __syncwarp();
+        if (lane < 16) {
+            const int p = lane >> 2, q = lane & 3;
+            double v = 0.0;
+#pragma unroll
+            for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+                for (int b2 = 0; b2 <= a2; ++b2) v = (a2 == p && b2 == q) ? l[a2][b2] : v;
+            lblk[b][p][q] = v;
+            if (q <= p && p < bw) A[(j + p) * ld + j + q] = v;
+            if (q == 0) {
+                double iv = 0.0;
+#pragma unroll
+                for (int a2 = 0; a2 < 4; ++a2) iv = (a2 == p) ? inv[a2] : iv;
+                linv[b][p] = iv;
+                if (p < bw) dinv[j + p] = iv;
             }
         }
-        __syncthreads();
+    };
+    if (wy == 0) factor_diag(0, 0);
+    __syncthreads();
+    for (int j = 0; j < N; j += 4) {
+        const int bw = min(4, N - j);
+        const int buf = (j >> 2) & 1;
         double l[4][4], inv[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            inv[p] = linv[p];
+            inv[p] = linv[buf][p];
 #pragma unroll
-            for (int q = 0; q < p; ++q) l[p][q] = lblk[p][q];
+            for (int q = 0; q < p; ++q) l[p][q] = lblk[buf][p][q];
         }
         for (int i = j + bw + tid; i <= N; i += kSmallThreads) {
             double x[4];
@@ -349,9 +355,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
                 }
         }
         __syncthreads();
+        const int jn = j + 4;                 // next diagonal block (look-ahead)
+        const int bwn = jn < N ? min(4, N - jn) : 0;
+        if (wy == 0) {
+            // warp 0: the next diagonal block's rank-4 update, then its factor,
+            // while the other warps update the rest of the trailing matrix
+            if (bwn > 0) {
+                if (lane < 16) {
+                    const int r = jn + (lane >> 2), c = jn + (lane & 3);
+                    if ((lane >> 2) < bwn && (lane & 3) <= (lane >> 2)) {
+                        double v = A[r * ld + c];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (q < bw) v -= colb[q][r] * colb[q][c];
+                        A[r * ld + c] = v;
+                    }
+                }
+                __syncwarp();
+                factor_diag(jn, buf ^ 1);
+            }
+            __syncthreads();
+            continue;
+        }
         // rank-4 update; a warp takes two rows at a time so each lane has two
         // independent FMA chains in flight (the loop is latency-bound)
-        for (int i0 = j + bw + 2 * wy; i0 <= N; i0 += 2 * ny) {
+        for (int i0 = jn + bwn + 2 * (wy - 1); i0 <= N; i0 += 2 * (ny - 1)) {
             const int i1 = i0 + 1;
             const bool two = i1 <= N;
             double la[4], lb[4];
