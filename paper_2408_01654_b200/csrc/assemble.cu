@@ -1018,6 +1018,50 @@ __global__ void __launch_bounds__(256) k_incidences2(int64_t I, const int32_t* _
     }
 }
 
+// small problems (few rows): one warp per row, lanes over the row's edges,
+// xor-tree reduction (fixed order)
+__global__ void k_rows_warp(int64_t P, const int32_t* row_ptr, const int32_t* row_pos,
+                            const double* e_terms, double* depth_diag, double* rhs_depth,
+                            uint8_t* active, double* cinv0, unsigned long long* grad_bits,
+                            unsigned long long* n_inactive) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double gmax = 0.0;
+    unsigned long long inact = 0;
+    for (int64_t r = warp; r < P; r += nwarps) {
+        double c = 0.0, g = 0.0;
+        for (int32_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) {
+            const double2 cg = __ldg(reinterpret_cast<const double2*>(
+                e_terms + (int64_t)__ldg(row_pos + k) * 8 + 6));
+            c += cg.x;
+            g += cg.y;
+        }
+        c = warp_sum(c);
+        g = warp_sum(g);
+        if (lane == 0) {
+            depth_diag[r] = c;
+            rhs_depth[r] = -g;
+            const bool act = c > kActiveEps;
+            active[r] = act ? 1 : 0;
+            cinv0[r] = act ? 1.0 / c : 0.0;
+            if (act) gmax = fmax(gmax, fabs(g));
+            else ++inact;
+        }
+    }
+    gmax = warp_max(gmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inact += __shfl_xor_sync(0xffffffffu, inact, o);
+    if (lane == 0) {
+        if (gmax > 0.0) {
+            const unsigned long long gb = (unsigned long long)__double_as_longlong(gmax);
+            atomicMax(grad_bits, gb);
+            atomicMax(grad_bits + 7, gb);
+        }
+        if (inact) atomicAdd(n_inactive, inact);
+    }
+}
+
 // coupling blocks per (var, row) incidence (ba.py:397-403)
 // uinc = inc_block * cinv0[row] (pair kernel) or, grouped, the symmetric
 // factor w = inc_block * sqrt(cinv0[row]) so the Schur blocks are sums of w w^T
@@ -1571,9 +1615,15 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
     auto* n_inactive = reinterpret_cast<unsigned long long*>(p->scal + 6);
     if (p->P > 0) {
         DPV_TSTART("rows", st);
-        k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,
-                                                     p->e_terms, p->depth_diag, p->rhs_depth,
-                                                     p->active, p->cinv0, grad_bits, n_inactive);
+        if (p->P < (int64_t)sm_count() * 64)      // few rows: a warp each
+            k_rows_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
+                p->P, p->row_ptr, p->row_pos, p->e_terms, p->depth_diag, p->rhs_depth,
+                p->active, p->cinv0, grad_bits, n_inactive);
+        else
+            k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,
+                                                         p->e_terms, p->depth_diag, p->rhs_depth,
+                                                         p->active, p->cinv0, grad_bits,
+                                                         n_inactive);
         DPV_CHECK_LAUNCH();
     }
     if (p->I > 0) {

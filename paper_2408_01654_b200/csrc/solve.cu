@@ -511,6 +511,34 @@ __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int3
     }
 }
 
+// small problems: one warp per row, lanes over the row's incidences
+__global__ void k_back_substitute_warp(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
+                                       const int32_t* inc_var, const double* inc_block,
+                                       const double* rhs_depth, const double* depth_diag,
+                                       const uint8_t* active, double lam, const double* dp,
+                                       double* dd) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < P; r += nwarps) {
+        double acc = 0.0;
+        for (int32_t k = rinc_ptr[r] + lane; k < rinc_ptr[r + 1]; k += 32) {
+            const int32_t i = __ldg(rinc + k);
+            const double* blk = inc_block + (int64_t)i * 6;
+            const double* x = dp + (int64_t)__ldg(inc_var + i) * 6;
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) s += __ldg(blk + a) * __ldg(x + a);
+            acc += s;
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const double cinv = active[r] ? 1.0 / (depth_diag[r] * (1.0 + lam)) : 0.0;
+            dd[r] = cinv * (rhs_depth[r] - acc);
+        }
+    }
+}
+
 __global__ void k_apply_step(int64_t F, int32_t first, int32_t last, int64_t P, const double* q,
                              const double* t, const double* d, const double* dp,
                              const double* dd, double* q2, double* t2, double* d2) {
@@ -790,9 +818,14 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
                         cudaStream_t st) {
     if (p->P == 0) return DPV_OK;
     DPV_TSTART("back_substitute", st);
-    k_back_substitute<<<grid_for(p->P, 256), 256, 0, st>>>(
-        p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
-        p->active, lam, dp, dd);
+    if (p->P < (int64_t)sm_count() * 64)           // few rows: a warp each
+        k_back_substitute_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
+            p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
+            p->active, lam, dp, dd);
+    else
+        k_back_substitute<<<grid_for(p->P, 256), 256, 0, st>>>(
+            p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
+            p->active, lam, dp, dd);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
 }
