@@ -121,10 +121,21 @@ class ClockSampler:
             try:
                 sm = p.nvmlDeviceGetClockInfo(self.handle, p.NVML_CLOCK_SM)
                 rs = p.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-                self.rows.append((sm, rs))
+                self.rows.append((sm, rs, time.perf_counter()))
             except Exception:
                 pass
             time.sleep(0.001)
+
+    # the thread is started (NVML initialised) before the warm-up; only the
+    # samples taken between mark_start() and mark_end() are summarised
+    t0 = None
+    t1 = None
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *exc):
         self.stop.set()
@@ -132,14 +143,18 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        if self.t0 is not None and self.t1 is not None:
+            rows = [r for r in rows if self.t0 <= r[2] <= self.t1]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         p = self.nvml
-        reasons = sorted({name for _, rs in self.rows for name, attr in self.NAMES
+        reasons = sorted({name for _, rs, _ in rows for name, attr in self.NAMES
                           if hasattr(p, attr) and rs & getattr(p, attr)})
-        sm = [r[0] for r in self.rows]
+        sm = [r[0] for r in rows]
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.max_sm),
-                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 1 ms polling"}
+                "reasons": reasons, "samples": len(rows),
+                "source": "NVML, 1 ms polling during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -518,6 +533,7 @@ def run_ours(args):
     else:
         st.lm_init()
         step_fn = st.lm_step
+    clk = ClockSampler(torch.cuda.current_device()).__enter__()
     for _ in range(max(args.warmup, 3)):
         step_fn()
     torch.cuda.synchronize()
@@ -545,11 +561,13 @@ def run_ours(args):
             graph = None
             torch.cuda.synchronize()
     launches0 = _lib.lib().dpv_launch_count()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        if graph is not None:
-            ms = time_steps(graph.replay, args.steps // 2, torch)
-        else:
-            ms = time_steps(step_fn, args.steps, torch)
+    clk.mark_start()
+    if graph is not None:
+        ms = time_steps(graph.replay, args.steps // 2, torch)
+    else:
+        ms = time_steps(step_fn, args.steps, torch)
+    clk.mark_end()
+    clk.__exit__(None, None, None)
     launches = _lib.lib().dpv_launch_count() - launches0
     if graph is not None:
         launches = per_graph * (args.steps // 2)
