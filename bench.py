@@ -328,6 +328,8 @@ class Stepper:
         if not late:
             k1()
         L.check(lib.dpv_assemble_rest(self.h, P(t), s), "assemble_rest")
+        if w["sharded"]:
+            w["prob"].allreduce_system()      # NCCL: the reduced pose system
         if late:
             k1()
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
@@ -336,6 +338,8 @@ class Stepper:
                                    P(t2), P(d2), s), "apply_step")
         L.check(lib.dpv_assemble_edges(self.h, P(q2), P(t2), P(d2), P(self.obj), s),
                 "assemble_edges")
+        if w["sharded"]:                      # the candidate objective: sum over shards
+            w["prob"].dist.all_reduce(self.obj, group=w["prob"].group)
         self.x, self.y = self.y, self.x
         torch.cuda.current_stream().wait_event(self.ev_join)
 
@@ -528,11 +532,8 @@ def run_ours(args):
     st = Stepper(work, torch)
     # device-resident step: one LM iteration with speculative assembly (the
     # native driver's flow); the sharded path keeps assemble + NCCL + objective
-    if work["sharded"]:
-        step_fn = st.step
-    else:
-        st.lm_init()
-        step_fn = st.lm_step
+    st.lm_init()
+    step_fn = st.lm_step
     clk = ClockSampler(torch.cuda.current_device()).__enter__()
     for _ in range(max(args.warmup, 3)):
         step_fn()
@@ -674,7 +675,10 @@ def run_ours(args):
                             "sparse solve, retraction, edge pass at the candidate = its "
                             "objective and the next iteration's terms; state advances) + K1 "
                             "on a side stream forked after the assembly") if not work["sharded"] else
-                           "assemble + NCCL all-reduce + solve + retraction + objective",
+                           ("one LM iteration on this rank's edge shard: rest of the assembly, "
+                            "all-reduce of the reduced pose system, redundant sparse solve, "
+                            "retraction, edge pass at the candidate + all-reduce of its "
+                            "objective; K1 beside it"),
                    "parallelism": (f"edge-shard x{world} by depth row, NCCL all-reduce of the "
                                    "reduced pose system" if world > 1 else "single GPU"),
                    "l2": f"inputs larger than L2 (flow targets {work['E'] * 144 / 1e9:.2f} GB, "
