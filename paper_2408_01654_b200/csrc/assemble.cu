@@ -1640,7 +1640,9 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
         DPV_CHECK_LAUNCH();
     }
     // few keys / vars: one CTA each (a warp each would leave most SMs idle)
-    const bool small = p->W < (int64_t)sm_count() * 8 && !p->grouped;
+    static const int kcta = getenv("DPV_KEY_CTA") ? atoi(getenv("DPV_KEY_CTA")) : -1;
+    const bool small = (kcta == 1 || (kcta != 0 && p->W < (int64_t)sm_count() * 8)) &&
+                       !p->grouped;
     if (p->W > 0 && small) {
         DPV_TSTART("key_blocks", st);
         k_key_blocks_cta<4><<<(int)p->W, 128, 0, st>>>(

@@ -818,7 +818,8 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
                         cudaStream_t st) {
     if (p->P == 0) return DPV_OK;
     DPV_TSTART("back_substitute", st);
-    if (p->P < (int64_t)sm_count() * 64)           // few rows: a warp each
+    static const int bw = getenv("DPV_BSUB_WARP") ? atoi(getenv("DPV_BSUB_WARP")) : -1;
+    if (bw == 1 || (bw != 0 && p->P < (int64_t)sm_count() * 64))   // few rows: a warp each
         k_back_substitute_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
             p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
             p->active, lam, dp, dd);
