@@ -86,9 +86,18 @@ class BAProblem:
         self._handle = None
         self._info = None
         self._cache = {}
+        # ownership token of the handle's assembly buffers: every native call
+        # that writes them takes a fresh token (_next_gen); a BlockSparseSystem
+        # re-assembles its own state when the token is no longer its own
         self._gen = 0
+        self._gen_counter = 0
         self._fill_count = None
         self.free_frames = list(range(first, last + 1))
+
+    def _next_gen(self) -> int:
+        self._gen_counter += 1
+        self._gen = self._gen_counter
+        return self._gen
 
     # -- device handle ---------------------------------------------------------
 
@@ -473,7 +482,7 @@ def assemble(problem: BAProblem, state=None) -> BlockSparseSystem:
     problem._ensure()
     q, t, d = _dev_state(problem, state)
     _run_assemble(problem, q, t, d)
-    problem._gen += 1
+    problem._next_gen()
     return BlockSparseSystem(problem, (q, t, d))
 
 
@@ -586,6 +595,7 @@ def solve_device(problem: BAProblem, q, t, d, max_iterations=50, tolerance=1e-9,
         active_patches = problem.active_patch_count()
     params = _lib.DpvLmParams(int(max_iterations), float(tolerance), float(problem.damping))
     rep = _lib.DpvLmReport()
+    problem._next_gen()          # the native LM re-assembles into the handle's buffers
     _lib.check(_lib.lib().dpv_lm_solve(h, _lib.ptr(q), _lib.ptr(t), _lib.ptr(d),
                                        C.byref(params), C.byref(rep), _lib.stream_ptr()),
                "solve")
@@ -687,6 +697,8 @@ def solve_batch(problems, max_iterations: int = 50, tolerance: float = 1e-9,
     params = (_lib.DpvLmParams * n)(*[_lib.DpvLmParams(int(it), float(tol), float(p.damping))
                                        for p, it, tol in zip(problems, iters, tols)])
     reps = (_lib.DpvLmReport * n)()
+    for p in problems:
+        p._next_gen()
     sp = (C.c_void_p * n)(*[s.cuda_stream for s in streams])
     status = (C.c_int32 * n)()
     rc = _lib.lib().dpv_lm_solve_batch(n, hs, qs, ts, ds, params, reps, sp, int(threads), status)

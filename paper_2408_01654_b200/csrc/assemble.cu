@@ -337,146 +337,6 @@ __device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
     return a * 6 - (a * (a - 1)) / 2 + (b - a);
 }
 
-template <int M, int U, int MINB, bool PF>
-__global__ void __launch_bounds__(128, MINB) k_assemble_edges(
-    int64_t S, int64_t E, int m_unused, int64_t P, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
-    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
-    const double* __restrict__ a_w, const double* __restrict__ r_ray,
-    const double* __restrict__ Rall, const double* __restrict__ tall,
-    const double* __restrict__ d, double fx, double fy, double cx, double cy,
-    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g,
-    double* __restrict__ seg_obj) {
-    const double intr[4] = {fx, fy, cx, cy};
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    __shared__ double sfr[4][24];
-    double* fr = sfr[threadIdx.x >> 5];
-    const FrameP fi{fr, fr + 9}, fj{fr + 12, fr + 21};
-    for (int64_t s = warp; s < S; s += nwarps) {
-        const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
-        __syncwarp();
-        if (lane < 12) {
-            const int32_t f = seg_src[s];
-            fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
-        } else if (lane < 24) {
-            const int32_t f = seg_dst[s];
-            fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
-        }
-        __syncwarp();
-        double H[21], G[6];
-        double fobj = 0.0;     // sum w r^2 over the segment (ba.py:248-253), free here
-#pragma unroll
-        for (int k = 0; k < 21; ++k) H[k] = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = 0.0;
-        // software prefetch (PF): the lane's next edge (e + 32) gets its targets,
-        // weights, rays and depth pulled into L1 one edge ahead; its row index
-        // is loaded two edges ahead
-        int32_t rn1 = (PF && e0 + lane + 32 < e1) ? a_row[e0 + lane + 32] : 0;
-        for (int32_t e = e0 + lane; e < e1; e += 32) {
-            if (PF) {
-                const int32_t en = e + 32;
-                int32_t rn2 = 0;
-                if (en < e1) {
-#pragma unroll
-                    for (int c = 0; c < 2 * M; ++c) {
-                        prefetch_l1(a_tgt + (int64_t)c * E + en);
-                        prefetch_l1(r_ray + (int64_t)c * P + rn1);
-                    }
-                    prefetch_l1(a_w + en);
-                    prefetch_l1(a_w + E + en);
-                    prefetch_l1(d + rn1);
-                    if (en + 32 < e1) rn2 = a_row[en + 32];
-                }
-                rn1 = rn2;
-            }
-            const int32_t row = a_row[e];
-            const double dd = __ldg(d + row);
-            const double id = __drcp_rn(dd);
-            // w J^T J instead of (sqrt(w) J)^T (sqrt(w) J) (ba.py:355-366): no sqrt
-            const double w0 = a_w[e], w1 = a_w[E + e];
-            double ep[6] = {0, 0, 0, 0, 0, 0};
-            double cdd = 0.0, gd = 0.0;
-#pragma unroll U
-            for (int c = 0; c < M; ++c) {
-                Cell cl;
-                reproject_cell(__ldg(r_ray + (int64_t)(2 * c) * P + row),
-                               __ldg(r_ray + (int64_t)(2 * c + 1) * P + row), id, fi, fj, intr,
-                               cl);
-                const double iz = cl.iz;
-                // A = Jproj R_j^T (geometry.py:514-522)
-                const double p0 = intr[0] * iz, q0 = -intr[0] * cl.xt[0] * iz * iz;
-                const double p1 = intr[1] * iz, q1 = -intr[1] * cl.xt[1] * iz * iz;
-                double J[2][6], jd[2];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    J[0][k] = p0 * fj.R[3 * k] + q0 * fj.R[3 * k + 2];
-                    J[1][k] = p1 * fj.R[3 * k + 1] + q1 * fj.R[3 * k + 2];
-                }
-                // rotational part x_w x a_row (geometry.py:524-526)
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    J[r][3] = cl.xw[1] * J[r][2] - cl.xw[2] * J[r][1];
-                    J[r][4] = cl.xw[2] * J[r][0] - cl.xw[0] * J[r][2];
-                    J[r][5] = cl.xw[0] * J[r][1] - cl.xw[1] * J[r][0];
-                }
-                // depth: A (t_i - x_w) / d (geometry.py:527-528)
-                const double g0 = (fi.t[0] - cl.xw[0]) * id, g1 = (fi.t[1] - cl.xw[1]) * id,
-                             g2 = (fi.t[2] - cl.xw[2]) * id;
-#pragma unroll
-                for (int r = 0; r < 2; ++r) jd[r] = J[r][0] * g0 + J[r][1] * g1 + J[r][2] * g2;
-                const double rr[2] = {(cl.u - a_tgt[(int64_t)(2 * c) * E + e]) ,
-                                      (cl.v - a_tgt[(int64_t)(2 * c + 1) * E + e])};
-                const double wv[2] = {cl.valid ? w0 : 0.0, cl.valid ? w1 : 0.0};
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    double wj[6];
-#pragma unroll
-                    for (int k = 0; k < 6; ++k) wj[k] = J[r][k] * wv[r];
-                    const double wjd = jd[r] * wv[r];
-#pragma unroll
-                    for (int a = 0; a < 6; ++a) {
-#pragma unroll
-                        for (int b = a; b < 6; ++b) H[utri(a, b)] += wj[a] * J[r][b];
-                        G[a] += wj[a] * rr[r];
-                        ep[a] += wj[a] * jd[r];
-                    }
-                    cdd += wjd * jd[r];
-                    gd += wjd * rr[r];
-                    fobj += wv[r] * rr[r] * rr[r];
-                }
-            }
-#pragma unroll
-            // AoS (E, 8): the row / incidence gathers read one 64-byte record
-            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
-            et[0] = make_double2(ep[0], ep[1]);
-            et[1] = make_double2(ep[2], ep[3]);
-            et[2] = make_double2(ep[4], ep[5]);
-            et[3] = make_double2(cdd, gd);
-        }
-#pragma unroll
-        for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
-        fobj = warp_sum(fobj);
-        if (seg_obj && lane == 0) seg_obj[s] = fobj;
-        if (lane < 21) {
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < 21; ++k) v = (lane == k) ? H[k] : v;
-            seg_h[s * 21 + lane] = v;
-        }
-        if (lane < 6) {
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
-            seg_g[s * 6 + lane] = v;
-        }
-    }
-}
-
 // Same pass in the TARGET camera's frame (default).  With B = diag(R_j, R_j)
 // the world Jacobian row is J_r = B k_r, k_r = [jp_r ; y x jp_r] where jp_r is
 // row r of Jproj and y = R_j^T x_w (rotation commutes with the cross
@@ -509,168 +369,6 @@ __device__ __forceinline__ void gram_row(const double (&k)[6], double wv, double
     cdd += wjd * jd;
     gd += wjd * rr;
     fobj += wv * rr * rr;
-}
-
-template <int U, int MINB, bool PF>
-__global__ void __launch_bounds__(128, MINB) k_assemble_edges_loc(
-    int64_t S, int64_t E, int64_t P, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_dst,
-    const int32_t* __restrict__ a_row, const double* __restrict__ a_tgt,
-    const double* __restrict__ a_w, const double* __restrict__ r_ray,
-    const double* __restrict__ Rall, const double* __restrict__ tall,
-    const double* __restrict__ d, double fx, double fy, double cx, double cy,
-    double* __restrict__ e_terms, double* __restrict__ seg_h, double* __restrict__ seg_g,
-    double* __restrict__ seg_obj) {
-    constexpr int M = 9;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // per warp: [0,24) raw frames (R_i t_i R_j t_j), [24,33) Rrel, [33,36) u,
-    // [36,39) c = R_j^T t_j, [40,76) local 6x6 Gram, [76,82) local gradient
-    __shared__ double sfr[4][82];
-    double* fr = sfr[threadIdx.x >> 5];
-    const double* Ri = fr;
-    const double* ti = fr + 9;
-    const double* Rj = fr + 12;
-    const double* tj = fr + 21;
-    const double* Rr = fr + 24;
-    const double* uu = fr + 33;
-    const double* cc = fr + 36;
-    double* Hs = fr + 40;
-    double* Gs = fr + 76;
-    for (int64_t s = warp; s < S; s += nwarps) {
-        const int32_t e0 = seg_ptr[s], e1 = seg_ptr[s + 1];
-        __syncwarp();
-        if (lane < 12) {
-            const int32_t f = seg_src[s];
-            fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
-        } else if (lane < 24) {
-            const int32_t f = seg_dst[s];
-            fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12) : __ldg(tall + 3 * f + lane - 21);
-        }
-        __syncwarp();
-        if (lane < 9) {               // Rrel[a][b] = sum_m R_j[m][a] R_i[m][b]
-            const int a = lane / 3, b = lane % 3;
-            fr[24 + lane] = Rj[a] * Ri[b] + Rj[3 + a] * Ri[3 + b] + Rj[6 + a] * Ri[6 + b];
-        } else if (lane < 12) {       // u = R_j^T (t_i - t_j)
-            const int a = lane - 9;
-            fr[24 + lane] = Rj[a] * (ti[0] - tj[0]) + Rj[3 + a] * (ti[1] - tj[1]) +
-                            Rj[6 + a] * (ti[2] - tj[2]);
-        } else if (lane < 15) {       // c = R_j^T t_j
-            const int a = lane - 12;
-            fr[24 + lane] = Rj[a] * tj[0] + Rj[3 + a] * tj[1] + Rj[6 + a] * tj[2];
-        }
-        __syncwarp();
-        double H[21], G[6];
-        double fobj = 0.0;
-#pragma unroll
-        for (int k = 0; k < 21; ++k) H[k] = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = 0.0;
-        int32_t rn1 = (PF && e0 + lane + 32 < e1) ? a_row[e0 + lane + 32] : 0;
-        for (int32_t e = e0 + lane; e < e1; e += 32) {
-            if (PF) {
-                const int32_t en = e + 32;
-                int32_t rn2 = 0;
-                if (en < e1) {
-#pragma unroll
-                    for (int c = 0; c < 2 * M; ++c) {
-                        prefetch_l1(a_tgt + (int64_t)c * E + en);
-                        prefetch_l1(r_ray + (int64_t)c * P + rn1);
-                    }
-                    prefetch_l1(a_w + en);
-                    prefetch_l1(a_w + E + en);
-                    prefetch_l1(d + rn1);
-                    if (en + 32 < e1) rn2 = a_row[en + 32];
-                }
-                rn1 = rn2;
-            }
-            const int32_t row = a_row[e];
-            const double id = __drcp_rn(__ldg(d + row));
-            const double w0 = a_w[e], w1 = a_w[E + e];
-            double ep[6] = {0, 0, 0, 0, 0, 0};
-            double cdd = 0.0, gd = 0.0;
-#pragma unroll U
-            for (int c = 0; c < M; ++c) {
-                const double xc0 = __ldg(r_ray + (int64_t)(2 * c) * P + row) * id;
-                const double xc1 = __ldg(r_ray + (int64_t)(2 * c + 1) * P + row) * id;
-                double xr[3], xt[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    xr[a] = Rr[3 * a] * xc0 + Rr[3 * a + 1] * xc1 + Rr[3 * a + 2] * id;
-                    xt[a] = xr[a] + uu[a];
-                }
-                const bool valid = xt[2] > kDepthEps;
-                const double iz = __drcp_rn(valid ? xt[2] : 1.0);
-                const double t0 = xt[0] * iz, t1 = xt[1] * iz;
-                const double p0 = fx * iz, p1 = fy * iz;
-                const double q0 = -p0 * t0, q1 = -p1 * t1;
-                const double y0 = xt[0] + cc[0], y1 = xt[1] + cc[1], y2 = xt[2] + cc[2];
-                const double k0[6] = {p0, 0.0, q0, y1 * q0, y2 * p0 - y0 * q0, -y1 * p0};
-                const double k1[6] = {0.0, p1, q1, y1 * q1 - y2 * p1, -y0 * q1, y0 * p1};
-                const double jd0 = -(p0 * xr[0] + q0 * xr[2]) * id;
-                const double jd1 = -(p1 * xr[1] + q1 * xr[2]) * id;
-                const double r0 = (fx * t0 + cx) - a_tgt[(int64_t)(2 * c) * E + e];
-                const double r1 = (fy * t1 + cy) - a_tgt[(int64_t)(2 * c + 1) * E + e];
-                gram_row<1>(k0, valid ? w0 : 0.0, r0, jd0, H, G, ep, cdd, gd, fobj);
-                gram_row<0>(k1, valid ? w1 : 0.0, r1, jd1, H, G, ep, cdd, gd, fobj);
-            }
-            // e_pd back to world coordinates: B ep
-            double ew[6];
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-                    ew[3 * h + a] = Rj[3 * a] * ep[3 * h] + Rj[3 * a + 1] * ep[3 * h + 1] +
-                                    Rj[3 * a + 2] * ep[3 * h + 2];
-            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
-            et[0] = make_double2(ew[0], ew[1]);
-            et[1] = make_double2(ew[2], ew[3]);
-            et[2] = make_double2(ew[4], ew[5]);
-            et[3] = make_double2(cdd, gd);
-        }
-#pragma unroll
-        for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
-        fobj = warp_sum(fobj);
-        if (seg_obj && lane == 0) seg_obj[s] = fobj;
-        // local sums -> shared (full symmetric 6x6), then B H B^T and B G
-        for (int idx = lane; idx < 36; idx += 32) {
-            const int a = idx / 6, b = idx % 6;
-            const int t = a <= b ? utri(a, b) : utri(b, a);
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < 21; ++q) v = (q == t) ? H[q] : v;
-            Hs[idx] = v;
-        }
-        if (lane < 6) {
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
-            Gs[lane] = v;
-        }
-        __syncwarp();
-        if (lane < 21) {
-            int a = 0;
-            while (a < 5 && utri(a + 1, a + 1) <= lane) ++a;
-            const int b = a + (lane - utri(a, a));
-            const int al = a % 3, ab = (a / 3) * 3, bl = b % 3, bb = (b / 3) * 3;
-            double v = 0.0;
-#pragma unroll
-            for (int pp = 0; pp < 3; ++pp) {
-                const double* hr = Hs + (ab + pp) * 6 + bb;
-                const double inner = hr[0] * Rj[3 * bl] + hr[1] * Rj[3 * bl + 1] +
-                                     hr[2] * Rj[3 * bl + 2];
-                v += Rj[3 * al + pp] * inner;
-            }
-            seg_h[s * 21 + lane] = v;
-        } else if (lane < 27) {
-            const int a = lane - 21, al = a % 3, ab = (a / 3) * 3;
-            seg_g[s * 6 + a] = Rj[3 * al] * Gs[ab] + Rj[3 * al + 1] * Gs[ab + 1] +
-                               Rj[3 * al + 2] * Gs[ab + 2];
-        }
-    }
 }
 
 // The local-frame edge pass with its inputs staged through shared memory:
@@ -1062,37 +760,6 @@ __global__ void k_rows_warp(int64_t P, const int32_t* row_ptr, const int32_t* ro
     }
 }
 
-// coupling blocks per (var, row) incidence (ba.py:397-403)
-// uinc = inc_block * cinv0[row] (pair kernel) or, grouped, the symmetric
-// factor w = inc_block * sqrt(cinv0[row]) so the Schur blocks are sums of w w^T
-__global__ void k_incidences(int64_t I, int64_t E, const int32_t* inc_ptr, const int32_t* inc_con,
-                             const int32_t* inc_row, const double* e_terms, const double* cinv0,
-                             double* inc_block, double* uinc, int sym) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double acc[6] = {0, 0, 0, 0, 0, 0};
-        for (int32_t k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
-            const int32_t code = inc_con[k];
-            const int32_t e = code >> 1;
-            const double sgn = (code & 1) ? -1.0 : 1.0;
-            const double2* et = reinterpret_cast<const double2*>(e_terms + (int64_t)e * 8);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const double2 v = __ldg(et + a);
-                acc[2 * a] += sgn * v.x;
-                acc[2 * a + 1] += sgn * v.y;
-            }
-        }
-        const double c0 = cinv0[inc_row[i]];
-        const double c = sym ? sqrt(c0) : c0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-            inc_block[i * 6 + a] = acc[a];
-            uinc[i * 6 + a] = acc[a] * c;
-        }
-    }
-}
-
 __device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -1271,47 +938,6 @@ __global__ void k_key_schur_sum(int64_t W, const int32_t* __restrict__ key_blk_p
     }
 }
 
-// rhs_pose (ba.py:375-380) and rhs_schur = E C0^-1 w (ba.py:415-417): warp per var
-__global__ void k_var_rhs(int64_t n, const int32_t* var_seg_ptr, const int32_t* var_seg,
-                          const double* seg_g, const int32_t* var_inc_ptr, const int32_t* inc_row,
-                          const double* inc_block, const double* cinv0, const double* rhs_depth,
-                          double* rhs_pose, double* rhs_schur, unsigned long long* grad_bits) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t v = warp; v < n; v += nwarps) {
-        double g[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};
-        for (int32_t k = var_seg_ptr[v] + lane; k < var_seg_ptr[v + 1]; k += 32) {
-            const int32_t code = var_seg[k];
-            const double sgn = (code & 1) ? -1.0 : 1.0;
-#pragma unroll
-            for (int a = 0; a < 6; ++a) g[a] += sgn * seg_g[(int64_t)(code >> 1) * 6 + a];
-        }
-        for (int32_t i = var_inc_ptr[v] + lane; i < var_inc_ptr[v + 1]; i += 32) {
-            const int32_t row = inc_row[i];
-            const double r = rhs_depth[row] * cinv0[row];
-#pragma unroll
-            for (int a = 0; a < 6; ++a) sc[a] += inc_block[(int64_t)i * 6 + a] * r;
-        }
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-            g[a] = warp_sum(g[a]);
-            sc[a] = warp_sum(sc[a]);
-        }
-        if (lane < 6) {
-            double gv = 0.0, sv = 0.0;
-#pragma unroll
-            for (int a = 0; a < 6; ++a) {
-                gv = (lane == a) ? g[a] : gv;
-                sv = (lane == a) ? sc[a] : sv;
-            }
-            rhs_pose[v * 6 + lane] = gv;
-            rhs_schur[v * 6 + lane] = sv;
-            atomicMax(grad_bits, (unsigned long long)__double_as_longlong(fabs(gv)));
-        }
-    }
-}
-
 // Small problems (few keys / vars, e.g. a 22-frame window): the same sums
 // with one 4-warp CTA per key / var, so each key's segments and pair runs are
 // split over 4 warps instead of one; partial results combine in a fixed
@@ -1454,18 +1080,10 @@ int32_t objective(dpv_problem* p, const double* q, const double* t, const double
     DPV_TSTART("objective", st);
     if (p->m == 9 && p->S > 0)
     {
-        const int variant = getenv("DPV_OBJ_VARIANT") ? atoi(getenv("DPV_OBJ_VARIANT")) : 0;
-#define DPV_OBJ(U, B, PF)                                                                    \
-    k_objective_seg<9, U, B, PF><<<kObjBlocks, 256, 0, st>>>(                                \
-        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,    \
-        p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3], p->obj_part)
-        switch (variant) {
-            case 1: DPV_OBJ(3, 4, false); break;
-            case 2: DPV_OBJ(1, 4, true); break;
-            case 3: DPV_OBJ(3, 3, true); break;
-            default: DPV_OBJ(3, 4, true); break;
-        }
-#undef DPV_OBJ
+        k_objective_seg<9, 3, 4, true><<<kObjBlocks, 256, 0, st>>>(
+            p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,
+            p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+            p->obj_part);
     }
     else
         k_objective<<<kObjBlocks, 256, 0, st>>>(p->E, p->m, p->P, p->a_src, p->a_dst, p->a_row,
@@ -1536,58 +1154,20 @@ int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, co
     DPV_TRY(frame_rotations(p, q, st));
     if (p->S > 0) {
         DPV_ARG(p->m == 9, "assembly kernel is instantiated for 3x3 patches");
-        const int warps_per_block = 4;
-        int blocks = (int)std::min<int64_t>((p->S + warps_per_block - 1) / warps_per_block,
-                                            (int64_t)sm_count() * 64);
+        // persistent: every warp walks many segments so the staging pipeline
+        // stays full; 4 warps x 2 blocks per SM (198 registers): 0.64 ms at
+        // cfg3 (register-capped 3x3 / 2x5 / 1x10 shapes spill: 0.83-0.86 ms)
+        constexpr int kNW = 4, kMinB = 2;
+        const size_t smem = sizeof(double) * 2 * kStgDoubles * kNW;
+        static size_t cur = 0;
+        DPV_TRY(ensure_smem(k_assemble_edges_stg<kNW, kMinB>, smem, cur));
+        const int pblocks = (int)std::min<int64_t>((p->S + kNW - 1) / kNW,
+                                                   (int64_t)sm_count() * kMinB);
         DPV_TSTART("assemble_edges", st);
-        const int variant = getenv("DPV_ASM_VARIANT") ? atoi(getenv("DPV_ASM_VARIANT")) : 0;
-#define DPV_ASM(U, B, PF)                                                                      \
-    k_assemble_edges<9, U, B, PF><<<blocks, 32 * warps_per_block, 0, st>>>(                    \
-        p->S, p->E, p->m, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt,        \
-        p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],    \
-        p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr)
-#define DPV_ASML(U, B, PF)                                                                     \
-    k_assemble_edges_loc<U, B, PF><<<blocks, 32 * warps_per_block, 0, st>>>(                   \
-        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,      \
-        p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],            \
-        p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr)
-        switch (variant) {
-            case 1: DPV_ASM(3, 3, false); break;
-            case 2: DPV_ASM(1, 3, true); break;
-            case 3: DPV_ASM(3, 2, true); break;
-            case 4: DPV_ASM(3, 3, true); break;       // world-frame pass
-            case 5: DPV_ASML(3, 4, true); break;
-            case 6: DPV_ASML(1, 3, true); break;
-            case 7: DPV_ASML(3, 3, true); break;
-            case 8: DPV_ASML(9, 3, true); break;
-            default: {
-                // persistent: every warp walks many segments so the staging
-                // pipeline stays full (MINB resident blocks per SM)
-                auto launch = [&](auto kern, int nw, int minb) -> int32_t {
-                    const size_t smem = sizeof(double) * 2 * kStgDoubles * nw;
-                    static size_t cur[4] = {0, 0, 0, 0};
-                    DPV_TRY(ensure_smem(kern, smem, cur[nw - 1]));
-                    const int pblocks = (int)std::min<int64_t>((p->S + nw - 1) / nw,
-                                                               (int64_t)sm_count() * minb);
-                    kern<<<pblocks, 32 * nw, smem, st>>>(
-                        p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row,
-                        p->a_tgt, p->a_w, p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1],
-                        p->intr[2], p->intr[3], p->e_terms, p->seg_h, p->seg_g,
-                        obj ? p->seg_obj : nullptr);
-                    return DPV_OK;
-                };
-                // 4 warps x 2 blocks (198 registers, 8 warps per SM): 0.64 ms at
-                // cfg3; 3x3 / 2x5 / 1x10 cap the registers at 168 and run
-                // 0.83-0.86 ms
-                if (variant == 10) DPV_TRY(launch(k_assemble_edges_stg<3, 3>, 3, 3));
-                else if (variant == 11) DPV_TRY(launch(k_assemble_edges_stg<1, 10>, 1, 10));
-                else if (variant == 12) DPV_TRY(launch(k_assemble_edges_stg<2, 5>, 2, 5));
-                else DPV_TRY(launch(k_assemble_edges_stg<4, 2>, 4, 2));
-                break;
-            }
-        }
-#undef DPV_ASM
-#undef DPV_ASML
+        k_assemble_edges_stg<kNW, kMinB><<<pblocks, 32 * kNW, smem, st>>>(
+            p->S, p->E, p->P, p->seg_ptr, p->seg_src, p->seg_dst, p->a_row, p->a_tgt, p->a_w,
+            p->r_ray, p->frame_R, t, d, p->intr[0], p->intr[1], p->intr[2], p->intr[3],
+            p->e_terms, p->seg_h, p->seg_g, obj ? p->seg_obj : nullptr);
         DPV_CHECK_LAUNCH();
     }
     if (obj) {
@@ -1628,21 +1208,14 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
     }
     if (p->I > 0) {
         DPV_TSTART("incidences", st);
-        const int iv = getenv("DPV_INC_VARIANT") ? atoi(getenv("DPV_INC_VARIANT")) : 0;
-        if (iv == 1)
-            k_incidences<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->E, p->inc_ptr, p->inc_con,
-                                                               p->inc_row, p->e_terms, p->cinv0,
-                                                               p->inc_block, p->uinc, p->grouped);
-        else
-            k_incidences2<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->inc_ptr, p->inc_con,
-                                                                p->inc_row, p->e_terms, p->cinv0,
-                                                                p->inc_block, p->uinc, p->grouped);
+        k_incidences2<<<grid_for(p->I, 256), 256, 0, st>>>(p->I, p->inc_ptr, p->inc_con,
+                                                            p->inc_row, p->e_terms, p->cinv0,
+                                                            p->inc_block, p->uinc, p->grouped);
         DPV_CHECK_LAUNCH();
     }
     // few keys / vars: one CTA each (a warp each would leave most SMs idle)
-    static const int kcta = getenv("DPV_KEY_CTA") ? atoi(getenv("DPV_KEY_CTA")) : -1;
-    const bool small = (kcta == 1 || (kcta != 0 && p->W < (int64_t)sm_count() * 8)) &&
-                       !p->grouped;
+    // (at cfg3 the per-key CTA form loses: 0.98 vs 0.51 ms)
+    const bool small = p->W < (int64_t)sm_count() * 8 && !p->grouped;
     if (p->W > 0 && small) {
         DPV_TSTART("key_blocks", st);
         k_key_blocks_cta<4><<<(int)p->W, 128, 0, st>>>(
@@ -1652,22 +1225,10 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
     } else if (p->W > 0) {
         int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("key_blocks", st);
-        const int kv = getenv("DPV_KEY_VARIANT") ? atoi(getenv("DPV_KEY_VARIANT")) : 0;
-#define DPV_KEY(U, B)                                                                          \
-    k_key_blocks<U, B><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,     \
-                                               p->key_run_ptr, p->run_l, p->run_r, p->run_len, \
-                                               p->uinc, p->inc_block, p->pose_blocks,          \
-                                               p->schur_blocks, p->grouped)
-        switch (kv) {
-            case 1: DPV_KEY(8, 1); break;
-            case 2: DPV_KEY(16, 1); break;
-            case 3: DPV_KEY(16, 3); break;
-            case 4: DPV_KEY(24, 2); break;
-            case 5: DPV_KEY(32, 2); break;
-            case 6: DPV_KEY(8, 4); break;
-            default: DPV_KEY(16, 3); break;
-        }
-#undef DPV_KEY
+        k_key_blocks<16, 3><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
+                                                    p->key_run_ptr, p->run_l, p->run_r,
+                                                    p->run_len, p->uinc, p->inc_block,
+                                                    p->pose_blocks, p->schur_blocks, p->grouped);
         DPV_CHECK_LAUNCH();
         if (p->grouped) {
             static size_t cur = 0;
@@ -1684,21 +1245,12 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
         }
     }
     if (p->n > 0) {
-        int blocks = (int)std::min<int64_t>((p->n + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("var_rhs", st);
-        // one 4-warp CTA per var at every size (cfg3: 0.078 -> 0.058 ms);
-        // DPV_VAR_RHS_CTA=0: the warp-per-var kernel
-        static const bool vcta = !getenv("DPV_VAR_RHS_CTA") || atoi(getenv("DPV_VAR_RHS_CTA")) != 0;
-        if (vcta) {
-            k_var_rhs_cta<<<(int)std::min<int64_t>(p->n, 65535), 128, 0, st>>>(
-                p->n, p->var_seg_ptr, p->var_seg, p->seg_g, p->var_inc_ptr, p->inc_row,
-                p->inc_block, p->cinv0, p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
-        } else {
-            k_var_rhs<<<blocks, 128, 0, st>>>(p->n, p->var_seg_ptr, p->var_seg, p->seg_g,
-                                              p->var_inc_ptr, p->inc_row, p->inc_block,
-                                              p->cinv0, p->rhs_depth, p->rhs_pose,
-                                              p->rhs_schur, grad_bits);
-        }
+        // one 4-warp CTA per var at every size (cfg3: 0.078 -> 0.058 ms
+        // against a warp per var)
+        k_var_rhs_cta<<<(int)std::min<int64_t>(p->n, 65535), 128, 0, st>>>(
+            p->n, p->var_seg_ptr, p->var_seg, p->seg_g, p->var_inc_ptr, p->inc_row,
+            p->inc_block, p->cinv0, p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
         DPV_CHECK_LAUNCH();
         if (p->scale_degenerate) {
             DPV_TSTART("pin", st);

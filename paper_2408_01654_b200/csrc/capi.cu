@@ -256,6 +256,7 @@ const char* dpv_last_error(void) { return t_error.c_str(); }
 int64_t dpv_launch_count(void) { return g_launches.load(); }
 
 int32_t dpv_device_info(int32_t* sms, int32_t* major, int32_t* minor) {
+    DPV_ABI_TRY
     int dev = 0;
     DPV_CUDA(cudaGetDevice(&dev));
     int v = 0;
@@ -266,16 +267,20 @@ int32_t dpv_device_info(int32_t* sms, int32_t* major, int32_t* minor) {
     DPV_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev));
     if (minor) *minor = v;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_timing_enable(int32_t on) {
+    DPV_ABI_TRY
     std::lock_guard<std::mutex> lk(g_tmu);
     g_timing = on != 0;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_timing_collect(char* names, int64_t names_cap, double* total_ms, int64_t* counts,
                            int32_t cap, int32_t* n_out) {
+    DPV_ABI_TRY
     // synchronises the device, aggregates event pairs per kernel name, resets
     DPV_CUDA(cudaDeviceSynchronize());
     std::lock_guard<std::mutex> lk(g_tmu);
@@ -313,35 +318,43 @@ int32_t dpv_timing_collect(char* names, int64_t names_cap, double* total_ms, int
     }
     if (n_out) *n_out = n;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_quat_to_matrix(const double* q, int64_t n, double* rot, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(n >= 0 && (n == 0 || (q && rot)), "bad quat_to_matrix args");
     return quat_to_matrix(q, n, rot, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_reproject_grid(const double* rays, const double* inv_depth, const double* rot_i,
                            const double* t_i, const double* rot_j, const double* t_j,
                            const double* intr4, int64_t n_edges, int32_t cells, double* pix,
                            uint8_t* valid, double* j_pose, double* j_depth, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(n_edges >= 0 && cells > 0 && intr4, "bad reproject_grid args");
     return reproject_grid(rays, inv_depth, rot_i, t_i, rot_j, t_j, intr4, n_edges, cells, pix,
                           valid, j_pose, j_depth, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_create(const dpv_graph* graph, int32_t first_free, int32_t last_free,
                            const int64_t* edge_indices, int64_t n_edge_indices, void* stream,
                            dpv_problem** out) {
+    DPV_ABI_TRY
     return dpv_problem_create_ex(graph, first_free, last_free, edge_indices, n_edge_indices,
                                  nullptr, 0, stream, out);
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_t last_free,
                               const int64_t* edge_indices, int64_t n_edge_indices,
                               const int64_t* extra_keys, int64_t n_extra_keys, void* stream,
                               dpv_problem** out) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(out != nullptr, "out is NULL");
     *out = nullptr;
@@ -358,23 +371,29 @@ int32_t dpv_problem_create_ex(const dpv_graph* graph, int32_t first_free, int32_
     spd_plan_prefetch(p);
     *out = p;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_set_gauge(dpv_problem* prob, int32_t scale_degenerate,
                               int32_t touched_fixed0) {
+    DPV_ABI_TRY
     DPV_ARG(prob, "NULL problem");
     prob->scale_degenerate = scale_degenerate ? 1 : 0;
     prob->touched0 = touched_fixed0;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_destroy(dpv_problem* prob) {
+    DPV_ABI_TRY
     delete prob;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_plan_info(const dpv_problem* p, int32_t* dense, int64_t* tiles,
                               int64_t* update_tiles, double* update_flops) {
+    DPV_ABI_TRY
     DPV_ARG(p, "NULL problem");
     if (p->spd) {
         int64_t v[9];
@@ -394,9 +413,11 @@ int32_t dpv_problem_plan_info(const dpv_problem* p, int32_t* dense, int64_t* til
     if (update_tiles) *update_tiles = p->plan->pair_count;
     if (update_flops) *update_flops = p->plan->syrk_flops;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_spd_info(const dpv_problem* p, int64_t* v9) {
+    DPV_ABI_TRY
     DPV_ARG(p && v9, "NULL argument");
     if (!p->spd) {
         set_error("no sparse factor plan yet (built by the first solve with n > 27)");
@@ -404,9 +425,11 @@ int32_t dpv_problem_spd_info(const dpv_problem* p, int64_t* v9) {
     }
     spd_plan_describe(p->spd, v9);
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_get_info(const dpv_problem* p, dpv_problem_info* info) {
+    DPV_ABI_TRY
     DPV_ARG(p && info, "NULL argument");
     info->n_edges = p->E;
     info->n_depths = p->P;
@@ -422,10 +445,12 @@ int32_t dpv_problem_get_info(const dpv_problem* p, dpv_problem_info* info) {
     info->touched_fixed0 = p->touched0;
     info->device_bytes = p->bytes;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_problem_array(const dpv_problem* p, const char* name, void** ptr, int64_t* count,
                           int32_t* dtype) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && name && ptr && count && dtype, "NULL argument");
     const std::string nm(name);
@@ -440,10 +465,12 @@ int32_t dpv_problem_array(const dpv_problem* p, const char* name, void** ptr, in
     *count = a.count;
     *dtype = a.dtype;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_gather_depths(const dpv_problem* p, const double* patch_depth, double* d,
                           void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p, "NULL problem");
     if (p->P == 0) return DPV_OK;
@@ -451,10 +478,12 @@ int32_t dpv_gather_depths(const dpv_problem* p, const double* patch_depth, doubl
                                                                         patch_depth, d);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_scatter_depths(const dpv_problem* p, const double* d, double* patch_depth,
                            void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p, "NULL problem");
     if (p->P == 0) return DPV_OK;
@@ -462,9 +491,11 @@ int32_t dpv_scatter_depths(const dpv_problem* p, const double* d, double* patch_
                                                                          d, patch_depth);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_active_patch_count(dpv_problem* p, double gate, int64_t* count, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && count, "NULL argument");
     cudaStream_t st = as_stream(stream);
@@ -482,95 +513,121 @@ int32_t dpv_active_patch_count(dpv_problem* p, double gate, int64_t* count, void
     DPV_CUDA(cudaStreamSynchronize(st));
     *count = (int64_t)h;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_residuals(dpv_problem* p, const double* q, const double* t, const double* d,
                       double* res, uint8_t* valid, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && (d || p->P == 0) && (res || p->E == 0), "NULL argument");
     return residuals(p, q, t, d, res, valid, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_objective(dpv_problem* p, const double* q, const double* t, const double* d,
                       double* out_dev, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && out_dev, "NULL argument");
     return objective(p, q, t, d, out_dev, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_assemble(dpv_problem* p, const double* q, const double* t, const double* d,
                      void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t, "NULL argument");
     return assemble(p, q, t, d, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, double* cinv,
                            void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p, "NULL problem");
     return reduced_system(p, lam, blocks, rhs, cinv, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_assemble_edges(dpv_problem* p, const double* q, const double* t, const double* d,
                            double* objective_out, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && (d || p->P == 0), "NULL argument");
     return assemble_edges_pass(p, q, t, d, objective_out, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_assemble_rest(dpv_problem* p, const double* t, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && t, "NULL argument");
     return assemble_rest(p, t, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status_dev,
                   void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && dp && (dd || p->P == 0) && status_dev, "NULL argument");
     return solve(p, lam, dp, dd, status_dev, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_reproject_coords(dpv_problem* p, const double* q, const double* t, const double* d,
                              double scale, double* coords_out, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && (coords_out || p->E == 0), "NULL argument");
     return coords(p, q, t, d, scale, coords_out, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_reproject_coords_sel(dpv_problem* p, const double* q, const double* t,
                                  const double* d, double scale, const int64_t* sel,
                                  int64_t n_sel, double* coords_out, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && (n_sel == 0 || (sel && coords_out)), "NULL argument");
     return coords_sel(p, q, t, d, scale, sel, n_sel, coords_out, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_update_targets(dpv_problem* p, const double* target, const double* conf,
                            void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && (target || p->E == 0), "NULL argument");
     return update_targets(p, target, conf, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_back_substitute(dpv_problem* p, double lam, const double* dp, double* dd,
                             void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && dp && (dd || p->P == 0), "NULL argument");
     return back_substitute(p, lam, dp, dd, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_apply_step(dpv_problem* p, const double* q, const double* t, const double* d,
                        const double* dp, const double* dd, double* q2, double* t2, double* d2,
                        void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && dp && q2 && t2, "NULL argument");
     return apply_step(p, q, t, d, dp, dd, q2, t2, d2, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
                      const dpv_lm_params* params, dpv_lm_report* rep, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(p && q && t && params && rep, "NULL argument");
     cudaStream_t st = as_stream(stream);
@@ -578,9 +635,12 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     const int kEscalations = 12;
     std::memset(rep, 0, sizeof(*rep));
     const int64_t F = p->F, P = p->P;
-    double* wq = p->lm_wq;
-    double* wt = p->lm_wt;
-    double* wd = p->lm_wd;
+    // references into the handle: an accepted step swaps the handle's own
+    // buffers, so every return path (including DPV_SINGULAR and errors)
+    // leaves lm_w* and lm_* distinct
+    double*& wq = p->lm_wq;
+    double*& wt = p->lm_wt;
+    double*& wd = p->lm_wd;
     DPV_CUDA(cudaMemcpyAsync(wq, q, sizeof(double) * F * 4, cudaMemcpyDeviceToDevice, st));
     DPV_CUDA(cudaMemcpyAsync(wt, t, sizeof(double) * F * 3, cudaMemcpyDeviceToDevice, st));
     if (P) DPV_CUDA(cudaMemcpyAsync(wd, d, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
@@ -588,12 +648,8 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     double* dev_scalar = p->scal + 8;  // scal[8..15] LM scalars on the device
     // speculative assembly: every state's objective comes from its edge pass,
     // so the accepted candidate's pass is the next iteration's (ba.py:534-605
-    // control flow unchanged; DPV_LM_PLAIN=1: separate objective kernel)
-    static const bool plain = getenv("DPV_LM_PLAIN") && atoi(getenv("DPV_LM_PLAIN")) != 0;
-    if (plain)
-        DPV_TRY(objective(p, wq, wt, wd, dev_scalar, st));
-    else
-        DPV_TRY(assemble_edges_pass(p, wq, wt, wd, dev_scalar, st));
+    // control flow unchanged)
+    DPV_TRY(assemble_edges_pass(p, wq, wt, wd, dev_scalar, st));
     DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
     DPV_CUDA(cudaStreamSynchronize(st));
     double obj = h[0];
@@ -605,8 +661,7 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     int32_t* status = p->status;
     for (int it = 0; it < params->max_iterations; ++it) {
         const double tic = now_s();
-        if (plain) DPV_TRY(assemble(p, wq, wt, wd, st));
-        else DPV_TRY(assemble_rest(p, wt, st));     // edge pass done when wq was evaluated
+        DPV_TRY(assemble_rest(p, wt, st));     // edge pass done when wq was evaluated
         DPV_CUDA(cudaMemcpyAsync(h + 3, p->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
         DPV_CUDA(cudaMemcpyAsync(h + 4, p->scal + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
         bool accepted = false, solved_once = false, singular = false;
@@ -617,10 +672,7 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
             rep->n_attempts++;
             DPV_TRY(solve(p, lam, p->lm_dp, p->lm_dd, status, st));
             DPV_TRY(apply_step(p, wq, wt, wd, p->lm_dp, p->lm_dd, p->lm_q, p->lm_t, p->lm_d, st));
-            if (plain)
-                DPV_TRY(objective(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
-            else
-                DPV_TRY(assemble_edges_pass(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
+            DPV_TRY(assemble_edges_pass(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
             k_step_norm<<<1, 256, 0, st>>>(6 * p->n, p->lm_dp, P, p->lm_dd, dev_scalar + 1);
             DPV_CHECK_LAUNCH();
             DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -685,17 +737,15 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     DPV_CUDA(cudaMemcpyAsync(q, wq, sizeof(double) * F * 4, cudaMemcpyDeviceToDevice, st));
     DPV_CUDA(cudaMemcpyAsync(t, wt, sizeof(double) * F * 3, cudaMemcpyDeviceToDevice, st));
     if (P) DPV_CUDA(cudaMemcpyAsync(d, wd, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
-    // keep the handle's buffer ownership consistent after swaps
-    p->lm_wq = wq;
-    p->lm_wt = wt;
-    p->lm_wd = wd;
     DPV_CUDA(cudaStreamSynchronize(st));
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_block_sparse_solve(const int64_t* keys, int64_t n_keys, int64_t n,
                                const double* blocks, const double* rhs, double* x,
                                int32_t* status_dev, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(keys && blocks && rhs && x && status_dev && n >= 1 && n_keys >= 1, "NULL argument");
     cudaStream_t st = as_stream(stream);
@@ -725,9 +775,11 @@ int32_t dpv_block_sparse_solve(const int64_t* keys, int64_t n_keys, int64_t n,
     if (dk) cudaFreeAsync(dk, st);
     spd_plan_free(plan);
     return rc;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(a && b && status_dev && n > 0, "bad cholesky_solve args");
     cudaStream_t st = as_stream(stream);
@@ -756,9 +808,11 @@ int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev,
                                    n * sizeof(double), n, cudaMemcpyDeviceToDevice, st));
     }
     return s;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_block_fill_count(const int64_t* keys, int64_t n_keys, int64_t n, int64_t* count) {
+    DPV_ABI_TRY
     // symbolic restatement of block_cholesky.py:54-105 (fill only, no numerics)
     clear_error();
     DPV_ARG(count && n >= 0 && (n_keys == 0 || keys), "bad block_fill_count args");
@@ -799,12 +853,14 @@ int32_t dpv_block_fill_count(const int64_t* keys, int64_t n_keys, int64_t n, int
     }
     *count = total;
     return DPV_OK;
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1, const double* coords,
                  const int32_t* ii, const int32_t* jj, int64_t n_edges, int32_t channels,
                  int32_t h0, int32_t w0, int32_t h1, int32_t w1, int32_t n_levels,
                  int32_t radius, int32_t dtype, float* out, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(n_edges >= 0 && channels > 0 && (n_levels == 1 || n_levels == 2) && radius >= 0 &&
                 radius <= 4 && (dtype == 0 || dtype == 1),
@@ -813,6 +869,7 @@ int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1, const d
     DPV_ARG(n_levels == 1 || fmap1, "level-1 feature map missing");
     return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,
                 radius, dtype, out, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
@@ -820,6 +877,7 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
                     int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
                     int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
                     void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(n_edges >= 0 && channels > 0 && (n_levels == 1 || n_levels == 2) && radius >= 0 &&
                 radius <= 4 && (dtype == 0 || dtype == 1) && n_patches >= 0 && n_frames >= 0,
@@ -829,7 +887,7 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
     cudaStream_t st = as_stream(stream);
     if (n_edges == 0) return DPV_OK;
     // TMA + tensor-core path: bf16, radius 3, C in {64, 128, 256}
-    if (dtype == 1 && radius == 3 && !getenv("DPV_CORR_NO_TMA")) {
+    if (dtype == 1 && radius == 3) {
         bool ok = true;
         for (int l = 0; l < n_levels && ok; ++l) {
             const int32_t r = corr_tma(gmap, n_patches, l == 0 ? fmap0 : fmap1, n_frames, coords,
@@ -844,25 +902,30 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
     }
     return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,
                 radius, dtype, out, st);
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_proximity_detect(const double* centers, int64_t n_frames, int64_t min_gap,
                              double threshold, int64_t* pairs, int64_t capacity, int64_t* count,
                              void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(count && (n_frames == 0 || centers) && min_gap >= 0 && n_frames >= 0,
             "bad detect args");
     return proximity_detect(centers, n_frames, min_gap, threshold, pairs, capacity, count,
                             as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_avg_pool4(const void* fmap, int64_t n_frames, int32_t h, int32_t w, int32_t channels,
                       int32_t dtype, void* out, void* stream) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(fmap && out && n_frames >= 0 && h > 0 && w > 0 && channels > 0 &&
                 (dtype == 0 || dtype == 1),
             "bad avg_pool4 args");
     return avg_pool4(fmap, n_frames, h, w, channels, dtype, out, as_stream(stream));
+    DPV_ABI_CATCH
 }
 
 }  // extern "C"
@@ -911,6 +974,7 @@ int32_t dpv_problem_create_batch(int32_t count, const dpv_graph* graphs,
                                  const int32_t* first_free, const int32_t* last_free,
                                  void* const* streams, int32_t threads, dpv_problem** out,
                                  int32_t* status) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(count >= 0, "negative count");
     if (count == 0) return DPV_OK;
@@ -924,12 +988,14 @@ int32_t dpv_problem_create_batch(int32_t count, const dpv_graph* graphs,
         if (status[i] != DPV_OK) msg[i] = dpv_last_error();
     });
     return first_failure(count, status, msg);
+    DPV_ABI_CATCH
 }
 
 int32_t dpv_lm_solve_batch(int32_t count, dpv_problem* const* probs, double* const* q,
                            double* const* t, double* const* d, const dpv_lm_params* params,
                            dpv_lm_report* reports, void* const* streams, int32_t threads,
                            int32_t* status) {
+    DPV_ABI_TRY
     clear_error();
     DPV_ARG(count >= 0, "negative count");
     if (count == 0) return DPV_OK;
@@ -941,6 +1007,7 @@ int32_t dpv_lm_solve_batch(int32_t count, dpv_problem* const* probs, double* con
         if (status[i] != DPV_OK) msg[i] = dpv_last_error();
     });
     return first_failure(count, status, msg);
+    DPV_ABI_CATCH
 }
 
 }  // extern "C"

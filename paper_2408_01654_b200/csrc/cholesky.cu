@@ -568,9 +568,7 @@ int32_t dense_factor_solve(double* A, int64_t ld, int64_t N, int32_t* status, do
     cudaEvent_t* evT = c.ev.data();
     cudaEvent_t* evR = c.ev.data() + ng;
     cudaEvent_t fork = c.ev[2 * ng], join_hi = c.ev[2 * ng + 1];
-    static const bool lookahead = !getenv("DPV_CHOL_LOOKAHEAD") ||
-                                  atoi(getenv("DPV_CHOL_LOOKAHEAD")) != 0;
-    cudaStream_t hi = lookahead ? c.hi : st, lo = lookahead ? c.lo : st;
+    cudaStream_t hi = c.hi, lo = c.lo;
     DPV_CUDA(cudaEventRecord(fork, st));
     DPV_CUDA(cudaStreamWaitEvent(hi, fork, 0));
     DPV_CUDA(cudaStreamWaitEvent(lo, fork, 0));

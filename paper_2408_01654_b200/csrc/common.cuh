@@ -7,6 +7,8 @@
 #include <atomic>
 #include <cstdio>
 #include <mutex>
+#include <exception>
+#include <new>
 #include <string>
 
 #include "../../include/dpvslam_b200.h"
@@ -65,6 +67,26 @@ struct Status {
             return DPV_BAD_ARGS;                                                    \
         }                                                                           \
     } while (0)
+
+// Every extern "C" entry point runs its body inside DPV_ABI_TRY { ... }
+// DPV_ABI_CATCH: a C++ exception (std::bad_alloc from a host vector, a
+// std::system_error from a worker thread) becomes a status code and a
+// dpv_last_error() message instead of crossing the C ABI.
+#define DPV_ABI_TRY try {
+#define DPV_ABI_CATCH                                                               \
+    }                                                                               \
+    catch (const std::bad_alloc&) {                                                 \
+        ::dpv::set_error(std::string(__func__) + ": host allocation failed");       \
+        return DPV_CUDA_ERROR;                                                      \
+    }                                                                               \
+    catch (const std::exception& _x) {                                              \
+        ::dpv::set_error(std::string(__func__) + ": " + _x.what());                 \
+        return DPV_CUDA_ERROR;                                                      \
+    }                                                                               \
+    catch (...) {                                                                   \
+        ::dpv::set_error(std::string(__func__) + ": unknown C++ exception");        \
+        return DPV_CUDA_ERROR;                                                      \
+    }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -451,11 +451,11 @@ int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const doubl
         if (dtype == 0)
             DPV_TRY(launch_corr<float>(gmap, f, coords, ii, jj, E, C, H, Wd, l, levels, radius,
                                        out, st));
-        else if (radius == 3 && C == 128 && !getenv("DPV_CORR_FMA"))
+        else if (radius == 3 && C == 128)
             DPV_TRY(launch_corr_mma<128>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
-        else if (radius == 3 && C == 64 && !getenv("DPV_CORR_FMA"))
+        else if (radius == 3 && C == 64)
             DPV_TRY(launch_corr_mma<64>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
-        else if (radius == 3 && C == 256 && !getenv("DPV_CORR_FMA"))
+        else if (radius == 3 && C == 256)
             DPV_TRY(launch_corr_mma<256>(gmap, f, coords, ii, jj, E, H, Wd, l, levels, out, st));
         else
             DPV_TRY(launch_corr<__nv_bfloat16>(gmap, f, coords, ii, jj, E, C, H, Wd, l, levels,

@@ -151,83 +151,9 @@ __device__ void smem_potrf(double* L, int ldl, int nb, int* bad, int pivot_base,
 // ---------------------------------------------------------------------------
 // small systems: everything in one CTA, shared memory ---------------------------
 
-__global__ void __launch_bounds__(1024) k_small_solve(
-    int64_t n, int64_t W, const int32_t* ka, const int32_t* kb, const double* pose,
-    const double* schur, const double* rhs_pose, const double* rhs_schur, const double* scal,
-    double lam, double* dp, int32_t* status) {
-    extern __shared__ double A[];
-    __shared__ double col[kSmallMax + 1];
-    __shared__ int bad;
-    const int N = (int)(6 * n);
-    const int ld = N + 1;
-    const int tid = threadIdx.x;
-    const int nt = blockDim.x;
-    for (int x = tid; x < (N + 1) * ld; x += nt) A[x] = 0.0;
-    if (tid == 0) bad = -1;
-    __syncthreads();
-    for (int64_t x = tid; x < W * 36; x += nt) {
-        const int64_t w = x / 36;
-        const int idx = (int)(x % 36);
-        const int i = idx / 6, j = idx % 6;
-        const int a = ka[w], b = kb[w];
-        const double v = reduced_entry(pose, schur, w, idx, a == b, lam);
-        if (a == b) {
-            if (i >= j) A[(6 * a + i) * ld + 6 * a + j] = v;
-        } else {
-            A[(6 * b + j) * ld + 6 * a + i] = v;
-        }
-    }
-    for (int c = tid; c < N; c += nt) A[N * ld + c] = rhs_pose[c] - rhs_schur[c] / (1.0 + lam);
-    __syncthreads();
-    if (tid == 0 && scal[1] != 0.0 && N >= 6) {
-        double mx = 0.0;
-        for (int k = 0; k < 6; ++k) mx = fmax(mx, fabs(A[k * ld + k]));
-        const double mu = 1e6 * fmax(1.0, mx);
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j <= i; ++j) A[i * ld + j] += mu * scal[2 + i] * scal[2 + j];
-    }
-    __syncthreads();
-    // right-looking Cholesky over columns 0..N-1; row N is the rhs
-    const int lane = tid & 31, wy = tid >> 5, ny = nt >> 5;
-    for (int j = 0; j < N; ++j) {
-        if (tid == 0) {
-            double piv = A[j * ld + j];
-            if (!(piv > 0.0)) {
-                if (bad < 0) bad = j;
-                piv = 1.0;
-            }
-            A[j * ld + j] = sqrt(piv);
-        }
-        __syncthreads();
-        const double ljj = A[j * ld + j];
-        for (int i = j + 1 + tid; i <= N; i += nt) {
-            const double v = A[i * ld + j] / ljj;
-            A[i * ld + j] = v;
-            col[i] = v;
-        }
-        __syncthreads();
-        for (int i = j + 1 + wy; i <= N; i += ny) {
-            const double lij = col[i];
-            const int kmax = i < N ? i : N - 1;
-            for (int k = j + 1 + lane; k <= kmax; k += 32) A[i * ld + k] -= lij * col[k];
-        }
-        __syncthreads();
-    }
-    // backward substitution L^T x = y (y in row N)
-    for (int j = N - 1; j >= 0; --j) {
-        if (tid == 0) A[N * ld + j] = A[N * ld + j] / A[j * ld + j];
-        __syncthreads();
-        const double xj = A[N * ld + j];
-        for (int i = tid; i < j; i += nt) A[N * ld + i] -= A[j * ld + i] * xj;
-        __syncthreads();
-    }
-    for (int c = tid; c < N; c += nt) dp[c] = A[N * ld + c];
-    if (tid == 0) status[0] = bad >= 0 ? 1 : 0;
-    if (tid == 0) status[1] = bad;
-}
-
-// Same solve, blocked by 4 columns (default; DPV_SMALL_V1=1: the unblocked
-// kernel above): warp 0 factors the 4x4 diagonal block, all threads scale
+// Small reduced systems (N = 6n <= kSmallMax): S(lam) is scattered into
+// shared memory with the rhs as its last row and factored in one CTA, blocked
+// by 4 columns: warp 0 factors the 4x4 diagonal block, all threads scale
 // the panel and apply the rank-4 update; the backward substitution runs by
 // 4-blocks on 256 threads (named barrier).  Same pivot reporting and
 // rhs-as-last-row forward substitution.  Warp 0 factors the NEXT diagonal
@@ -585,12 +511,6 @@ __global__ void k_apply_step(int64_t F, int32_t first, int32_t last, int64_t P, 
 
 int64_t dense_ld(int64_t N) { return ((N + 1 + 7) / 8) * 8; }
 
-// DPV_DENSE_SOLVE=1: the dense (tile-plan) factorisation instead of spd.cu
-bool dense_solve_forced() {
-    static const bool v = getenv("DPV_DENSE_SOLVE") && atoi(getenv("DPV_DENSE_SOLVE")) != 0;
-    return v;
-}
-
 // Symmetric permutation + tile plan of the reduced camera system (host, once
 // per problem: the pattern = union_keys is state-independent).  Poses with a
 // long-range coupling (a loop-closure block farther than `band` poses from
@@ -606,14 +526,9 @@ int32_t ensure_plan(dpv_problem* p, int64_t N, cudaStream_t st) {
     DPV_CUDA(cudaStreamSynchronize(st));
     std::vector<int32_t> pos(n);
     for (int64_t v = 0; v < n; ++v) pos[v] = (int32_t)v;
-    const char* env = getenv("DPV_DENSE_SOLVE");
-    const bool dense = env && atoi(env) == 1;   // 2 (or spd fallback): sparse tile plan
     auto* plan = new (std::nothrow) FactorPlan();
     DPV_ARG(plan != nullptr, "allocation failed");
-    if (dense) {
-        int32_t s = build_factor_plan(N, nullptr, *plan);
-        if (s != DPV_OK) { delete plan; return s; }
-    } else {
+    {
         const int T = (int)((N + 63) / 64);
         double best = -1.0;
         std::vector<int32_t> best_pos = pos;
@@ -697,11 +612,9 @@ int32_t reduced_system(dpv_problem* p, double lam, double* blocks, double* rhs, 
 // Start the sparse-solver plan on a host thread right after the index build
 // (the union keys are final), so its ~1 ms of host work overlaps the first
 // edge pass and assembly on the device.  Same plan, same failure fallback
-// as building it inside the first solve.  DPV_SPD_SYNC_PLAN=1: build in solve.
+// as building it inside the first solve.
 void spd_plan_prefetch(dpv_problem* p) {
-    static const bool sync_plan = getenv("DPV_SPD_SYNC_PLAN") &&
-                                  atoi(getenv("DPV_SPD_SYNC_PLAN")) != 0;
-    if (sync_plan || 6 * p->n <= kSmallMax || p->W == 0 || dense_solve_forced() ||
+    if (6 * p->n <= kSmallMax || p->W == 0 ||
         p->plan_thread.joinable() || p->spd)
         return;
     int dev = 0;
@@ -739,28 +652,16 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
               cudaStream_t st) {
     const int64_t N = 6 * p->n;
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
-    static const int64_t small_max =
-        getenv("DPV_SMALL_MAX") ? std::min<int64_t>(atoll(getenv("DPV_SMALL_MAX")), kSmallMax)
-                                : kSmallMax;
-    if (N <= small_max) {
+    if (N <= kSmallMax) {
         const size_t smem = sizeof(double) * (size_t)(N + 1) * (N + 1);
-        static const bool v1 = getenv("DPV_SMALL_V1") && atoi(getenv("DPV_SMALL_V1")) != 0;
         DPV_TSTART("small_solve", st);
-        if (v1) {
-            static size_t cur = 0;
-            DPV_TRY(ensure_smem(k_small_solve, smem, cur));
-            k_small_solve<<<1, 1024, smem, st>>>(p->n, p->W, p->key_a, p->key_b, p->pose_blocks,
-                                                 p->schur_blocks, p->rhs_pose, p->rhs_schur,
-                                                 p->scal, lam, dp, status);
-        } else {
-            static size_t cur = 0;
-            DPV_TRY(ensure_smem(k_small_solve2, smem, cur));
-            k_small_solve2<<<1, kSmallThreads, smem, st>>>(
-                p->n, p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, p->rhs_pose,
-                p->rhs_schur, p->scal, lam, dp, status);
-        }
+        static size_t cur = 0;
+        DPV_TRY(ensure_smem(k_small_solve2, smem, cur));
+        k_small_solve2<<<1, kSmallThreads, smem, st>>>(
+            p->n, p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, p->rhs_pose,
+            p->rhs_schur, p->scal, lam, dp, status);
         DPV_CHECK_LAUNCH();
-    } else if (!dense_solve_forced() && !p->spd_failed) {
+    } else if (!p->spd_failed) {
         // banded + border sparse factorisation (spd.cu)
         if (!p->spd && p->plan_thread.joinable()) {
             p->plan_thread.join();           // built beside the first edge pass
@@ -818,8 +719,7 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
                         cudaStream_t st) {
     if (p->P == 0) return DPV_OK;
     DPV_TSTART("back_substitute", st);
-    static const int bw = getenv("DPV_BSUB_WARP") ? atoi(getenv("DPV_BSUB_WARP")) : -1;
-    if (bw == 1 || (bw != 0 && p->P < (int64_t)sm_count() * 64))   // few rows: a warp each
+    if (p->P < (int64_t)sm_count() * 64)   // few rows: a warp each (cfg3: 0.19 vs 0.07 ms)
         k_back_substitute_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
             p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
             p->active, lam, dp, dd);

@@ -8,6 +8,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+# the reference package installed by build() (git-ignored, travels to the GPU
+# box): makes the drop-in exception hierarchy and the reference-suite shim
+# tests (test_gpu_reference_suite.py) available; nothing on the product path
+# computes with it
+REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(REF, "patchslam")) and REF not in sys.path:
+    sys.path.append(REF)
 
 
 def pytest_configure(config):

@@ -1,0 +1,57 @@
+"""Drop-in proof: the reference's own hot-path test modules, UNCHANGED, pass
+with this package installed as the hot path (``shim.install``).
+
+The reference package and its tests are staged by ``build()`` into the
+git-ignored ``baseline/_ref`` (``patchslam`` via an offline pip install,
+``reference_tests/`` copied from pkg/tests), which travels to the GPU box.
+Each module runs in a fresh interpreter with ``-p _reference_shim``; the plugin
+patches ``patchslam.ba`` / ``geometry`` / ``graph`` / ``synthetic`` /
+``block_cholesky`` (the list in shim.py) before the test modules import, and
+reports how many of this package's kernels ran.
+
+Modules (VERDICT r1 "Next round" 3): test_ba.py (LM, Schur vs
+full normal equations, dense vs block-sparse, SingularSystem escalation),
+test_block_cholesky.py, test_geometry.py (reprojection and Jacobians vs finite
+differences), test_loop.py (global BA after closure).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+REF_TESTS = os.path.join(REF, "reference_tests")
+if not os.path.isdir(os.path.join(REF, "patchslam")) or not os.path.isdir(REF_TESTS):
+    pytest.skip("reference package not staged in baseline/_ref (run build())",
+                allow_module_level=True)
+
+MODULES = ["test_ba.py", "test_block_cholesky.py", "test_geometry.py", "test_loop.py"]
+
+
+@pytest.mark.parametrize("module", MODULES)
+def test_reference_module_passes_through_shim(module, tmp_path):
+    report = tmp_path / "shim.json"
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([ROOT, REF, env.get("PYTHONPATH", ""),
+                                         os.path.join(ROOT, "tests")])
+    env["DPV_SHIM_REPORT"] = str(report)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "_reference_shim",
+           "--rootdir", REF_TESTS, "-c", os.devnull, os.path.join(REF_TESTS, module)]
+    out = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True,
+                         timeout=1200)
+    tail = (out.stdout + out.stderr)[-4000:]
+    assert out.returncode == 0, tail
+    assert " passed" in out.stdout, tail
+    launches = json.load(open(report))["launches"]
+    assert launches > 0, "no kernels of this package ran: the shim was not used"
+    print(f"{module}: {out.stdout.strip().splitlines()[-1]}; {launches} kernel launches")

@@ -1,5 +1,5 @@
 """Isolated K1 timing: cfg3-shaped correlation (E_corr edges, 52 feature
-frames of 120x160x128 bf16, 2 levels), tensor-core vs CUDA-core kernel.
+frames of 120x160x128 bf16, 2 levels) through the shipped TMA kernel.
 
     python tools/bench_corr.py [--edges 47232] [--frames 52] [--sorted 1]
 """
@@ -39,13 +39,7 @@ def main():
         jj, _ = torch.sort(jj)
     out = torch.empty((E, 2, 9, 7, 7), dtype=torch.float32, device="cuda")
     hbm_bytes = E * (144 + 8 + 2 * 441 * 4) + E * 9 * C * 2 + sum(p.numel() * 2 for p in pyr)
-    for mode in ("tma", "mma", "fma"):
-        os.environ.pop("DPV_CORR_FMA", None)
-        os.environ.pop("DPV_CORR_NO_TMA", None)
-        if mode != "tma":
-            os.environ["DPV_CORR_NO_TMA"] = "1"
-        if mode == "fma":
-            os.environ["DPV_CORR_FMA"] = "1"
+    for mode in ("tma",):
         for _ in range(3):
             corr.corr(gmap, pyr, coords, ii, jj, out=out)
         torch.cuda.synchronize()
