@@ -449,20 +449,13 @@ def kernel_rooflines(timing, work, steps, hbm_peak):
 # CPU baseline: the numpy oracle port on a bounded sample
 
 
-def cpu_sample(work, sample_frames=40, corr_edges=1500, dense_solve=True):
-    import scipy.linalg
-    from oracle import ba_oracle as O
+REF_PREFIX = 250     # frames of the cfg3 graph in the reference arm's sub-problem
+
+
+def corr_cpu_sample(work, corr_edges=1500):
+    """The correlation lookup has no reference code: its CPU
+    figure is the float64 numpy oracle port on a bounded sample."""
     from oracle import corr_oracle
-    g = work["graph"].soa()
-    soa = {k: np.array(v) for k, v in g.items()}
-    t0 = time.perf_counter()
-    prob = O.OracleProblem(soa, (1, sample_frames))
-    state = prob.state()
-    obj = O.objective(prob, state)
-    O.assemble(prob, state)
-    t_ba = time.perf_counter() - t0
-    e_s = len(prob.edge_indices)
-    # correlation: same feature shapes, float64 numpy
     rng = np.random.default_rng(0)
     C = work["C"]
     fm = rng.normal(size=(4, work["H0"], work["W0"], C)) / math.sqrt(C)
@@ -473,33 +466,70 @@ def cpu_sample(work, sample_frames=40, corr_edges=1500, dense_solve=True):
     t0 = time.perf_counter()
     corr_oracle.corr(gm, fms, coords, rng.integers(0, 64, corr_edges),
                      rng.integers(0, 4, corr_edges))
-    t_corr = time.perf_counter() - t0
-    N = 6 * int(work["info"].n_free)
-    t_solve = 0.0
-    Ns = min(N, 12000)          # LAPACK at N > 12k: time 12k, scale by (N/12k)^3
-    if dense_solve:
-        N, Nfull = Ns, N
-        a = rng.random((N, N))
-        a = a + a.T
-        a[np.diag_indices(N)] += 2.0 * N + 1.0
-        b = rng.random(N)
+    dt = time.perf_counter() - t0
+    return {"value": corr_edges / dt, "unit": "corr-edges/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/corr_oracle.py (numpy f64) on {corr_edges} edges, 2 levels, C={C}"}
+
+
+def cpu_sample(work, steps=1, warmup=0):
+    """CPU baseline on this host: the unmodified reference (bench_ref.py) when
+    it is installed in baseline/_ref, else the numpy oracle port, running full
+    LM iterations of the named sub-problem (the first REF_PREFIX frames of the
+    same graph).  value = its edges per second; nothing is extrapolated."""
+    import bench_ref
+    g = work["graph"].soa()
+    soa = {k: np.array(v) for k, v in g.items()}
+    if bench_ref.reference_available():
+        r = bench_ref.time_iterations(soa, REF_PREFIX, steps, warmup)
+        kind = "reference"
+    else:
+        r = port_iterations(soa, REF_PREFIX, steps, warmup)
+        kind = "port"
+    out = {"value": r["value"], "unit": "patch-edges/s", "cores": r["cores"], "kind": kind,
+           "sample": r["sample"], "step_s": r["step_s"], "E_sample": r["E"],
+           "setup_s": r["setup_s"], "objectives": r["objectives"]}
+    try:
+        out["corr_port"] = corr_cpu_sample(work)
+    except Exception as exc:            # reported, not fatal
+        out["corr_port"] = {"error": repr(exc)}
+    return out
+
+
+def port_iterations(soa, prefix, steps, warmup):
+    """Same step as bench_ref.time_iterations through the oracle port
+    (oracle/ba_oracle.py, pinned to the reference's golden vectors)."""
+    from oracle import ba_oracle as O
+    nf = prefix
+    keep = (soa["edge_src"] < nf) & (soa["edge_dst"] < nf)
+    sub = dict(soa)
+    for k in ("edge_src", "edge_patch", "edge_dst", "edge_target", "edge_conf", "edge_kind"):
+        sub[k] = soa[k][keep]
+    sub["frame_q"], sub["frame_t"] = soa["frame_q"][:nf], soa["frame_t"][:nf]
+    t0 = time.perf_counter()
+    prob = O.OracleProblem(sub, (1, nf - 1))
+    prob.structure()
+    prob.maps()
+    setup_s = time.perf_counter() - t0
+    backend = O.select_backend(prob)
+    solver = O.solve_dense if backend == "dense" else O.solve_block_sparse
+    q, t, d = prob.state()
+    times, objs = [], []
+    for i in range(warmup + steps):
         t0 = time.perf_counter()
-        cho = scipy.linalg.cho_factor(a, check_finite=False)
-        scipy.linalg.cho_solve(cho, b, check_finite=False)
-        t_solve = (time.perf_counter() - t0) * (Nfull / N) ** 3
-        N = Nfull
-    E = work["E"]
-    Ec = len(work["csel"])
-    step_s = t_ba / e_s * E + t_corr / corr_edges * Ec + t_solve
-    return {
-        "value": E / step_s, "unit": "patch-edges/s", "cores": os.cpu_count(), "kind": "port",
-        "step_s": step_s, "objective_sample": obj,
-        "sample": (f"oracle (numpy f64) objective+assemble on BAProblem(1,{sample_frames}) of the "
-                   f"same graph ({e_s} edges, {t_ba:.2f}s) scaled to E={E}; corr oracle on "
-                   f"{corr_edges} edges ({t_corr:.2f}s) scaled to E_corr={Ec}; LAPACK "
-                   f"cho_factor+cho_solve at N={min(N, Ns)} scaled to N={N} ({t_solve:.2f}s, "
-                   f"OpenBLAS threads)"),
-    }
+        system = O.assemble(prob, (q, t, d))
+        dp, dd, _ = solver(system, prob.damping)
+        q, t, d = O.apply_step(q, t, d, dp, dd, prob)
+        obj = O.objective(prob, (q, t, d))
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+            objs.append(obj)
+    E = len(prob.edge_indices)
+    step_s = float(np.median(times))
+    return {"E": E, "step_s": step_s, "setup_s": setup_s, "objectives": objs,
+            "value": E / step_s, "cores": os.cpu_count(), "step_times_s": times,
+            "sample": (f"oracle port (numpy f64): one LM iteration per step on the global BA over "
+                       f"the first {prefix} frames of the cfg3 graph (E = {E}); median of "
+                       f"{len(times)} after {warmup} warm-up")}
 
 
 # ---------------------------------------------------------------------------
@@ -616,6 +646,15 @@ def run_ours(args):
         roof["note"] = notes[dominant[0]]
     serial_ms = sum(v["ms_per_step"] for v in kernels.values())
     roof["serialised_kernel_ms"] = serial_ms
+    # step-level HBM fraction: SURVEY 8(d) algorithmic bytes of one LM
+    # iteration (2 edge passes x 172 B, 2 x 24 B per patch, incidences
+    # written + read, pose / Schur blocks, rhs) over the measured step
+    inf = work["info"]
+    step_bytes = (2 * 172 * work["E"] + 48 * int(inf.n_depths)
+                  + 96 * int(getattr(inf, "n_inc", 0)) + 288 * int(getattr(inf, "n_keys", 0))
+                  + 48 * int(inf.n_free))
+    roof["step_algorithmic_bytes"] = step_bytes
+    roof["step_hbm_frac"] = step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak
 
     # e2e through the C-ABI from pinned host buffers
     e2e = None
@@ -670,6 +709,10 @@ def run_ours(args):
                    "corr_levels": 2, "corr_channels": work["C"], "corr_dtype": args.feat_dtype,
                    "feature_frames": work["n_feat_frames"],
                    "lm_attempt_per_step": 1,
+                   "step_kind": ("device-only LM iteration replayed as a CUDA graph: fixed lambda, "
+                                 "the candidate is always accepted, no host read-back; the native "
+                                 "driver's per-iteration time (host accept test, lambda "
+                                 "escalation) is global_ba.iteration_ms"),
                    "cuda_graph": graph is not None,
                    "step": ("one LM iteration (speculative assembly: rest of the assembly at x, "
                             "sparse solve, retraction, edge pass at the candidate = its "
@@ -689,6 +732,8 @@ def run_ours(args):
         "factor_plan": work.get("plan"),
         "index_build_ms": work["build_ms"],
         "global_ba": glob,
+        "lm_solve_iteration_ms": (float(np.median(glob["iteration_ms"]))
+                                  if glob and glob.get("iteration_ms") else None),
         "window_step": window,
         "window_step_cfg1": window1,
         "batch_replicas": batch,
@@ -1090,46 +1135,42 @@ def run_global(work, args, torch):
 
 
 def run_reference(args):
-    """Reference arm: the reference algorithm restated in numpy (oracle/, the
-    reference itself is pure Python and cannot travel to this box) on the
-    host cores, bounded sample per step of the same workload."""
+    """Reference arm: the unmodified reference package (baseline/_ref) on the
+    host cores -- each step one full LM iteration of the named sub-problem of
+    the same workload (bench_ref.py); the numpy oracle port if the reference
+    is not installed.  Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import torch  # noqa: F401  (only for the shared workload builder's graph)
+    import bench_ref
     from paper_2408_01654_b200 import synthetic
     t0 = time.perf_counter()
     scene, graph, free = synthetic.make_config(args.config)
     gen_s = time.perf_counter() - t0
-    from oracle import ba_oracle as O
     soa = {k: np.array(v) for k, v in graph.soa().items()}
-    full = O.OracleProblem(soa, free)
-    E = len(full.edge_indices)
-    nf = graph.n_frames
-    dst = soa["edge_dst"][full.edge_indices]
-    kind = soa["edge_kind"][full.edge_indices]
-    Ec = int(((dst >= nf - args.window) | (kind == 1)).sum())
-    work = {"graph": graph, "E": E, "C": args.channels, "H0": scene.spec.image_size[1] // 4,
-            "W0": scene.spec.image_size[0] // 4, "csel": np.zeros(Ec),
-            "info": type("I", (), {"n_free": free[1] - free[0] + 1})()}
-    samples = []
-    for i in range(max(args.warmup, 0) + args.steps):
-        s = cpu_sample(work, dense_solve=True)
-        if i >= args.warmup:
-            samples.append(s)
-    step_s = float(np.median([s["step_s"] for s in samples]))
-    value = E / step_s
-    cb = dict(samples[-1])
-    cb["value"] = value
+    prefix = min(REF_PREFIX, graph.n_frames)
+    warm = max(args.warmup, 0)
+    if bench_ref.reference_available():
+        r = bench_ref.time_iterations(soa, prefix, args.steps, warm)
+        kind = "reference"
+    else:
+        r = port_iterations(soa, prefix, args.steps, warm)
+        kind = "port"
+    value = r["value"]
     return {
         "impl": "reference",
         "metric": "patch-edges/sec for corr lookup + Gauss-Newton BA step; global loop-closure BA ms",
         "value": value, "unit": "patch-edges/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "warmup": warm, "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bit-exactly)",
-        "config": {"workload": f"{args.config} (same as the ours arm)", "E_ba": E, "E_corr": Ec},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": {"workload": (f"{args.config} graph, global BA over its first {prefix} frames "
+                                f"(the bounded sample; the ours arm runs all {graph.n_frames})"),
+                   "E_ba": r["E"], "E_corr": 0,
+                   "corr": "none: the reference has no correlation code (SPEC.md:14)"},
+        "cpu_baseline": {"value": value, "unit": "patch-edges/s", "cores": r["cores"],
+                         "kind": kind, "sample": r["sample"]},
+        "reference_run": {k: r[k] for k in ("step_times_s", "objectives", "setup_s")},
         "e2e": {"value": value, "unit": "patch-edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "input_generation_s": gen_s,

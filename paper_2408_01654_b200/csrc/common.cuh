@@ -31,6 +31,7 @@ struct Status {
     do {                                                                            \
         cudaError_t _e = (expr);                                                    \
         if (_e != cudaSuccess) {                                                    \
+            (void)cudaGetLastError(); /* a non-sticky error must not resurface */   \
             ::dpv::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) +   \
                              " @ " + __FILE__ + ":" + std::to_string(__LINE__));    \
             return DPV_CUDA_ERROR;                                                  \

@@ -851,7 +851,7 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         uint64_t* ukey;
         int32_t* counts;
         DPV_TRY(sc.get(&ukey, NC));
-        DPV_TRY(sc.get(&counts, NC));
+        DPV_TRY(sc.get(&counts, NC + 1));     // + the scan's terminating zero (I == NC possible)
         DPV_TRY(cub_run(sc, [&](void* t, size_t& b) {
             return cub::DeviceRunLengthEncode::Encode(t, b, cks, ukey, counts, dcount, (int)NC,
                                                       st);
