@@ -888,16 +888,9 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
     if (n_edges == 0) return DPV_OK;
     // TMA + tensor-core path: bf16, radius 3, C in {64, 128, 256}
     if (dtype == 1 && radius == 3) {
-        bool ok = true;
-        for (int l = 0; l < n_levels && ok; ++l) {
-            const int32_t r = corr_tma(gmap, n_patches, l == 0 ? fmap0 : fmap1, n_frames, coords,
-                                       ii, jj, n_edges, channels, l == 0 ? h0 : h1,
-                                       l == 0 ? w0 : w1, l, n_levels, out, st);
-            if (r == DPV_CUDA_ERROR) return r;
-            ok = r == DPV_OK;
-            if (!ok && l > 0) return r;     // level 0 already written: no mixed paths
-        }
-        if (ok) return DPV_OK;
+        const int32_t r = corr_tma(gmap, n_patches, fmap0, fmap1, n_frames, coords, ii, jj,
+                                   n_edges, channels, h0, w0, h1, w1, n_levels, out, st);
+        if (r != DPV_BAD_ARGS) return r;
         clear_error();
     }
     return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,

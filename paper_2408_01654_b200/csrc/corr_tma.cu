@@ -123,29 +123,46 @@ __device__ __forceinline__ void split(double v, int& i0, float& fr) {
     fr = (float)(v - f);
 }
 
+// Per-NH (C / 64 channel halves) pipeline shape: stage bytes (window halves,
+// patch-feature halves, item metadata; 1024-aligned for the 128B swizzle),
+// NS stages in the ring, NG consumer groups of 4 warps (each group works on
+// its own item, so NG items are in flight per SM besides the prefetched ones).
 template <int NH>
-constexpr int stage_bytes() {
-    return ((NH * (kHalfBytes + kGHalfBytes) + (int)sizeof(ItemMeta) + 1023) / 1024) * 1024;
+struct CorrCfg {
+    static constexpr int SB =
+        ((NH * (kHalfBytes + kGHalfBytes) + (int)sizeof(ItemMeta) + 1023) / 1024) * 1024;
+    static constexpr int NS = (200 * 1024) / SB < 8 ? (200 * 1024) / SB : 8;
+    static constexpr int NG = NS - 1 < 4 ? NS - 1 : 4;
+    static constexpr int kThreadsT = 32 + NG * kConsumers;
+    static constexpr size_t kSmem =
+        (size_t)NS * SB + sizeof(float) * NG * kCellsT * kTapsPad + 1024;
+};
+
+__device__ __forceinline__ void bar_group(int g) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "n"(kConsumers) : "memory");
 }
 
+// One persistent CTA per SM; items are (edge, level) pairs, level fastest, so
+// both pyramid levels run in ONE launch.  Warp 0 is the TMA producer, warps
+// 1.. form NG consumer groups; local item k goes to stage k % NS and group
+// k % NG.
 template <int NH>
-__global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
-    const __grid_constant__ CUtensorMap fmap_map, const __grid_constant__ CUtensorMap gmap_map,
-    const __nv_bfloat16* __restrict__ fmap, const __nv_bfloat16* __restrict__ gmap,
+__global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, 1) k_corr_tma(
+    const __grid_constant__ CUtensorMap fmap0_map, const __grid_constant__ CUtensorMap fmap1_map,
+    const __grid_constant__ CUtensorMap gmap_map, const __nv_bfloat16* __restrict__ fmap0,
+    const __nv_bfloat16* __restrict__ fmap1, const __nv_bfloat16* __restrict__ gmap,
     const double* __restrict__ coords, const int32_t* __restrict__ ii,
-    const int32_t* __restrict__ jj, int64_t E, int H, int Wd, int level, int levels,
+    const int32_t* __restrict__ jj, int64_t E, int h0, int w0, int h1, int w1, int levels,
     float* __restrict__ out) {
-    constexpr int C = 64 * NH;
-    constexpr int SB = stage_bytes<NH>();
-    extern __shared__ __align__(16) unsigned char smem_raw[];   // aligned to 1024 below
-    // 1024-byte aligned stage ring
-    // (pointer arithmetic on the shared array keeps the shared address space)
+    using Cfg = CorrCfg<NH>;
+    constexpr int C = 64 * NH, SB = Cfg::SB, NS = Cfg::NS, NG = Cfg::NG;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // 1024-byte aligned stage ring (pointer arithmetic keeps the shared space)
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    float* S = reinterpret_cast<float*>(sm + kStages * SB);          // 9 x kTapsPad
-    __shared__ uint64_t full[kStages], empty[kStages];
+    __shared__ uint64_t full[NS], empty[NS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumers);
         }
@@ -154,19 +171,18 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
     __syncthreads();
     // grid-stride items: the CTAs work on neighbouring edges at any time, so
     // the target frames' feature maps stay L2-resident (edges grouped by frame)
-    const int64_t n_my = E > blockIdx.x ? (E - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const double scale = level == 0 ? 1.0 : 0.25;
+    const int64_t NV = E * levels;
+    const int64_t n_my = NV > blockIdx.x ? (NV - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     constexpr int radius = 3, D = 8, O = 7;
 
-    if (warp == kProducerWarp) {
+    if (warp == 0) {
         // ---------------- producer ----------------
-        // the next item's coordinates and indices are loaded one item ahead,
-        // so their latency overlaps the current item's hand-off
+        // the next item's coordinates and indices are loaded one item ahead
         double cxn = 0.0, cyn = 0.0;
         int32_t iin = 0, jjn = 0;
         auto fetch = [&](int64_t u) {
             if (u >= n_my) return;
-            const int64_t e = blockIdx.x + u * (int64_t)gridDim.x;
+            const int64_t e = (blockIdx.x + u * (int64_t)gridDim.x) / levels;
             if (lane < kCellsT) {
                 cxn = __ldg(coords + (e * kCellsT + lane) * 2);
                 cyn = __ldg(coords + (e * kCellsT + lane) * 2 + 1);
@@ -178,13 +194,16 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
         };
         fetch(0);
         for (int64_t u = 0; u < n_my; ++u) {
-            const int64_t e = blockIdx.x + u * (int64_t)gridDim.x;
-            const int s = (int)(u % kStages);
+            const int64_t v = blockIdx.x + u * (int64_t)gridDim.x;
+            const int64_t e = v / levels;
+            const int level = (int)(v - e * levels);
+            const int s = (int)(u % NS);
             const double cx = cxn, cy = cyn;
             const int32_t iic = iin, jjc = jjn;
             fetch(u + 1);
-            mbar_wait(&empty[s], (unsigned)(((u / kStages) & 1) ^ 1));
+            mbar_wait(&empty[s], (unsigned)(((u / NS) & 1) ^ 1));
             ItemMeta* M = reinterpret_cast<ItemMeta*>(sm + s * SB + NH * (kHalfBytes + kGHalfBytes));
+            const double scale = level == 0 ? 1.0 : 0.25;
             int x0 = 0, y0 = 0;
             float fx = 0.f, fy = 0.f;
             if (lane < kCellsT) {
@@ -204,20 +223,15 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
             const bool staged = (mxx - mnx) <= kWin - D && (mxy - mny) <= kWin - D &&
                                 mnx > -(1 << 27);
             if (lane < kCellsT) {
-                M->cell[lane].ox = x0 - radius - bx0;
-                M->cell[lane].oy = y0 - radius - by0;
+                M->cell[lane].ox = staged ? x0 - radius - bx0 : x0 - radius;
+                M->cell[lane].oy = staged ? y0 - radius - by0 : y0 - radius;
                 M->cell[lane].fx = fx;
                 M->cell[lane].fy = fy;
-                // per-cell origin for the slow path
-                if (!staged) {
-                    M->cell[lane].ox = x0 - radius;
-                    M->cell[lane].oy = y0 - radius;
-                }
             }
             if (lane == 0) {
                 M->bx0 = bx0;
                 M->by0 = by0;
-                M->staged = staged ? 1 : 0;
+                M->staged = (staged ? 1 : 0) | (level << 1);
                 M->jj = jjc;
                 M->e = e;
             }
@@ -227,18 +241,20 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
                 const unsigned tx = NH * kGHalfBytes + (staged ? NH * kWin * kWin * 128 : 0);
                 mbar_arrive_tx(&full[s], tx);
                 const int grow = iic * kCellsT;
+                const CUtensorMap* fm = level == 0 ? &fmap0_map : &fmap1_map;
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     tma_2d(st + NH * kHalfBytes + h * kGHalfBytes, &gmap_map, 64 * h, grow,
                            &full[s]);
-                    if (staged)
-                        tma_4d(st + h * kHalfBytes, &fmap_map, 64 * h, bx0, by0, M->jj, &full[s]);
+                    if (staged) tma_4d(st + h * kHalfBytes, fm, 64 * h, bx0, by0, jjc, &full[s]);
                 }
             }
         }
         return;
     }
-    // ---------------- consumers (4 warps) ----------------
+    // ---------------- consumer groups (4 warps each) ----------------
+    const int grp = (warp - 1) >> 2, gw = (warp - 1) & 3, gtid = tid - 32 - grp * kConsumers;
+    float* S = reinterpret_cast<float*>(sm + NS * SB) + grp * (kCellsT * kTapsPad);
     const int g = lane >> 2, t4 = lane & 3;
     // ldmatrix lane roles (128B swizzle: chunk' = chunk ^ (row % 8), rows of
     // a tile start 1024-aligned so row % 8 = lane % 8 for every matrix):
@@ -247,25 +263,26 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
     const int l7 = lane & 7;
     const unsigned offA = (unsigned)((l7 + 8 * ((lane >> 3) & 1)) * 128);
     const unsigned mA = (unsigned)(((lane >> 4) ^ l7) << 4);
-    const unsigned offB = (unsigned)((warp * 8 + l7) * 128);
+    const unsigned offB = (unsigned)((gw * 8 + l7) * 128);
     const unsigned mB = (unsigned)(((lane >> 3) ^ l7) << 4);
-    // blend slots of this thread (x = tid + 128 i < 441), fixed for all items
+    // blend slots of this thread (x = gtid + 128 i < 441), fixed for all items
     int slot_c[4], slot_off[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const int x = tid + kConsumers * i;
+        const int x = gtid + kConsumers * i;
         const int c = x / (O * O), ab = x % (O * O);
         slot_c[i] = x < kCellsT * O * O ? c : -1;
         slot_off[i] = c * kTapsPad + (ab / O) * kWin + ab % O;
     }
-    for (int64_t u = 0; u < n_my; ++u) {
-        const int s = (int)(u % kStages);
-        mbar_wait(&full[s], (unsigned)((u / kStages) & 1));
+    for (int64_t u = grp; u < n_my; u += NG) {
+        const int s = (int)(u % NS);
+        mbar_wait(&full[s], (unsigned)((u / NS) & 1));
         const unsigned char* st = sm + s * SB;
         const ItemMeta* M = reinterpret_cast<const ItemMeta*>(st + NH * (kHalfBytes + kGHalfBytes));
         const unsigned char* Gs = st + NH * kHalfBytes;
+        const int level = M->staged >> 1;
         float* o = out + ((M->e * levels + level) * kCellsT) * (int64_t)(O * O);
-        if (M->staged) {
+        if (M->staged & 1) {
             float acc[4][4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
@@ -280,7 +297,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
                     ldsm_x4(a1, gb + ((unsigned)((kc + 2) << 4) ^ mA));
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        if (warp + 4 * q < 13) {
+                        if (gw + 4 * q < 13) {
                             uint32_t b[4];
                             ldsm_x4(b, wb + q * 4096 + ((unsigned)(kc << 4) ^ mB));
                             mma_bf16_t(acc[q], a0, b[0], b[1]);
@@ -291,32 +308,32 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int nt = warp + 4 * q;
+                const int nt = gw + 4 * q;
                 if (nt < 13) {
                     const int col = nt * 8 + 2 * t4;
-                    S[g * kTapsPad + col] = acc[q][0];
-                    S[g * kTapsPad + col + 1] = acc[q][1];
-                    if (g == 0) {
-                        S[8 * kTapsPad + col] = acc[q][2];
-                        S[8 * kTapsPad + col + 1] = acc[q][3];
-                    }
+                    *reinterpret_cast<float2*>(S + g * kTapsPad + col) =
+                        make_float2(acc[q][0], acc[q][1]);
+                    if (g == 0)
+                        *reinterpret_cast<float2*>(S + 8 * kTapsPad + col) =
+                            make_float2(acc[q][2], acc[q][3]);
                 }
             }
-            bar_consumers();
+            bar_group(grp);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 if (slot_c[i] < 0) continue;
                 const CellMeta cm = M->cell[slot_c[i]];
                 const float* sp = S + slot_off[i] + cm.oy * kWin + cm.ox;
-                o[tid + kConsumers * i] =
+                o[gtid + kConsumers * i] =
                     (1.f - cm.fy) * ((1.f - cm.fx) * sp[0] + cm.fx * sp[1]) +
                     cm.fy * ((1.f - cm.fx) * sp[kWin] + cm.fx * sp[kWin + 1]);
             }
         } else {
             // wide or non-finite window: per-cell integer-tap dots from global memory
-            const __nv_bfloat16* fp = fmap + (int64_t)M->jj * H * Wd * C;
+            const int H = level == 0 ? h0 : h1, Wd = level == 0 ? w0 : w1;
+            const __nv_bfloat16* fp = (level == 0 ? fmap0 : fmap1) + (int64_t)M->jj * H * Wd * C;
             const __nv_bfloat16* gp = gmap + (int64_t)ii[M->e] * kCellsT * C;
-            for (int x = tid; x < kCellsT * D * D; x += kConsumers) {
+            for (int x = gtid; x < kCellsT * D * D; x += kConsumers) {
                 const int c = x / (D * D), ty = (x % (D * D)) / D, tx = x % D;
                 const int py = M->cell[c].oy + ty, px = M->cell[c].ox + tx;
                 float acc = 0.f;
@@ -327,8 +344,8 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
                 }
                 S[c * kTapsPad + ty * D + tx] = acc;
             }
-            bar_consumers();
-            for (int x = tid; x < kCellsT * O * O; x += kConsumers) {
+            bar_group(grp);
+            for (int x = gtid; x < kCellsT * O * O; x += kConsumers) {
                 const int c = x / (O * O), ab = x % (O * O), a = ab / O, bb = ab % O;
                 const float dx = M->cell[c].fx, dy = M->cell[c].fy;
                 const float* sp = S + c * kTapsPad + a * D + bb;
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 2) k_corr_tma(
                        dy * ((1.f - dx) * sp[D] + dx * sp[D + 1]);
             }
         }
-        bar_consumers();          // S and the stage are free
+        bar_group(grp);          // S and the stage are free
         mbar_arrive(&empty[s]);
     }
 }
@@ -356,24 +373,32 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-// bf16 features, radius 3, C in {64, 128, 256}; returns DPV_BAD_ARGS when the
-// TMA path does not apply (the caller falls back to corr.cu)
-int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap, int64_t n_frames,
-                 const double* coords, const int32_t* ii, const int32_t* jj, int64_t E, int C,
-                 int H, int Wd, int level, int levels, float* out, cudaStream_t st) {
+// bf16 features, radius 3, C in {64, 128, 256}, both levels in one launch;
+// returns DPV_BAD_ARGS when the TMA path does not apply (the caller falls
+// back to corr.cu)
+int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                 int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                 int64_t E, int C, int h0, int w0, int h1, int w1, int levels, float* out,
+                 cudaStream_t st) {
     auto enc = encode_fn();
     if (!enc || (C != 64 && C != 128 && C != 256) || n_patches < 1 || n_frames < 1 ||
-        (reinterpret_cast<uintptr_t>(fmap) & 15) || (reinterpret_cast<uintptr_t>(gmap) & 15))
+        (levels == 2 && (!fmap1 || h1 < 1 || w1 < 1)) ||
+        (reinterpret_cast<uintptr_t>(fmap0) & 15) || (reinterpret_cast<uintptr_t>(gmap) & 15) ||
+        (levels == 2 && (reinterpret_cast<uintptr_t>(fmap1) & 15)))
         return DPV_BAD_ARGS;
-    CUtensorMap fm, gm;
-    {
+    CUtensorMap fm[2], gm;
+    for (int l = 0; l < 2; ++l) {
+        // level 1 absent: encode level 0 twice (never read)
+        const bool has = l < levels;
+        const int H = has && l == 1 ? h1 : h0, Wd = has && l == 1 ? w1 : w0;
+        const void* f = has && l == 1 ? fmap1 : fmap0;
         const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)Wd, (cuuint64_t)H,
                                     (cuuint64_t)n_frames};
         const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)Wd * C * 2,
                                        (cuuint64_t)H * Wd * C * 2};
         const cuuint32_t box[4] = {64, kWin, kWin, 1};
         const cuuint32_t es[4] = {1, 1, 1, 1};
-        if (enc(&fm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(fmap), dims, strides,
+        if (enc(&fm[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(f), dims, strides,
                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS)
@@ -390,26 +415,23 @@ int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap, int64_t 
             CUDA_SUCCESS)
             return DPV_BAD_ARGS;
     }
-    auto launch = [&](auto kern, int sb) -> int32_t {
-        const size_t smem = (size_t)kStages * sb + sizeof(float) * kCellsT * kTapsPad + 1024;
+    auto launch = [&](auto kern, size_t smem, int threads, int slot) -> int32_t {
         static size_t cur[3] = {0, 0, 0};
-        const int slot = C == 64 ? 0 : (C == 128 ? 1 : 2);
         DPV_TRY(ensure_smem(kern, smem, cur[slot]));
-        int per_sm = 0;
-        DPV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kConsumers + 32,
-                                                               smem));
-        const int64_t want = (int64_t)sm_count() * std::max(1, per_sm);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(E, want));
+        const int64_t items = E * levels;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, sm_count()));
         DPV_TSTART("corr", st);
-        kern<<<grid, kConsumers + 32, smem, st>>>(fm, gm, reinterpret_cast<const __nv_bfloat16*>(fmap),
-                                                  reinterpret_cast<const __nv_bfloat16*>(gmap),
-                                                  coords, ii, jj, E, H, Wd, level, levels, out);
+        kern<<<grid, threads, smem, st>>>(fm[0], fm[1], gm,
+                                          reinterpret_cast<const __nv_bfloat16*>(fmap0),
+                                          reinterpret_cast<const __nv_bfloat16*>(fmap1),
+                                          reinterpret_cast<const __nv_bfloat16*>(gmap), coords,
+                                          ii, jj, E, h0, w0, h1, w1, levels, out);
         DPV_CHECK_LAUNCH();
         return DPV_OK;
     };
-    if (C == 64) return launch(k_corr_tma<1>, stage_bytes<1>());
-    if (C == 128) return launch(k_corr_tma<2>, stage_bytes<2>());
-    return launch(k_corr_tma<4>, stage_bytes<4>());
+    if (C == 64) return launch(k_corr_tma<1>, CorrCfg<1>::kSmem, CorrCfg<1>::kThreadsT, 0);
+    if (C == 128) return launch(k_corr_tma<2>, CorrCfg<2>::kSmem, CorrCfg<2>::kThreadsT, 1);
+    return launch(k_corr_tma<4>, CorrCfg<4>::kSmem, CorrCfg<4>::kThreadsT, 2);
 }
 
 }  // namespace dpv

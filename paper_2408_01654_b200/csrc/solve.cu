@@ -300,9 +300,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
                 __syncwarp();
                 factor_diag(jn, buf ^ 1);
             }
-            __syncthreads();
-            continue;
-        }
+        } else {
         // rank-4 update; a warp takes two rows at a time so each lane has two
         // independent FMA chains in flight (the loop is latency-bound)
         for (int i0 = jn + bwn + 2 * (wy - 1); i0 <= N; i0 += 2 * (ny - 1)) {
@@ -336,7 +334,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
                 }
             }
         }
-        __syncthreads();
+        }   // warps 1..: trailing update
+        __syncthreads();   // one barrier site for every warp
     }
     // backward substitution L^T x = y (y in row N) by blocks of 4: every
     // thread solves the block's 4x4 triangle redundantly, then the earlier

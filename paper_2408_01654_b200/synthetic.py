@@ -320,12 +320,19 @@ def make_flow_oracle(scene, config: OracleConfig, seed: int = 0):
     return oracle
 
 
-def perturb_poses(graph, sigma: float, seed: int, first: int = 1) -> None:
+def perturb_poses(graph, sigma: float, seed: int, first: int = 1, frame: str = "world") -> None:
     """Left-multiply Pose.exp(N(0, sigma)) onto every frame from ``first``
-    (pkg/tests/conftest.py:28-32)."""
+    (pkg/tests/conftest.py:28-32).  ``frame="camera"`` right-multiplies the
+    same draws instead (a perturbation about each camera centre), which keeps
+    the perturbation local on a scene far from the world origin (cfg4: a
+    world-frame 0.02 rad rotation moves a camera 440 m out by metres)."""
+    if frame not in ("world", "camera"):
+        raise ValueError(f"unknown perturbation frame {frame!r}")
     rng = np.random.default_rng(seed)
     for f in range(first, graph.n_frames):
-        p = Pose.exp(rng.normal(0, sigma, 6)) * Pose(graph._q.view[f], graph._t.view[f])
+        cur = Pose(graph._q.view[f], graph._t.view[f])
+        noise = Pose.exp(rng.normal(0, sigma, 6))
+        p = noise * cur if frame == "world" else cur * noise
         graph._q.view[f] = p.q
         graph._t.view[f] = p.t
     graph._pose_ver += 1
@@ -364,7 +371,7 @@ CONFIGS = {
                            look="forward", image_size=(1226, 370),
                            intrinsics=Intrinsics(718.856, 718.856, 607.193, 185.216),
                            extent=440.0),
-                 loops=4500, free=lambda n: (1, n - 1)),
+                 loops=4500, free=lambda n: (1, n - 1), perturb="camera"),
 }
 
 DESCRIPTIONS = {
@@ -395,5 +402,5 @@ def make_config(name: str, initial_targets: bool = False, seed: int | None = Non
     if cfg["loops"]:
         add_loop_edges(graph, cfg["loops"], 96, seed=0)
     fill_flow(graph, scene, OracleConfig(pixel_noise_sigma=0.3), seed=1)
-    perturb_poses(graph, 0.02, seed=11)
+    perturb_poses(graph, 0.02, seed=11, frame=cfg.get("perturb", "world"))
     return scene, graph, cfg["free"](spec.n_frames)

@@ -71,11 +71,13 @@ def graph_soa(graph) -> dict:
     return out
 
 
-def perturb_poses(graph, sigma, seed, first=1):
-    # restated from the reference test conftest (pkg/tests/conftest.py:28-32)
+def perturb_poses(graph, sigma, seed, first=1, frame="world"):
+    # restated from the reference test conftest (pkg/tests/conftest.py:28-32);
+    # frame="camera" right-multiplies the same draws (the cfg4 recipe)
     rng = np.random.default_rng(seed)
     for f in graph.frames[first:]:
-        f.pose = Pose.exp(rng.normal(0, sigma, 6)) * f.pose
+        noise = Pose.exp(rng.normal(0, sigma, 6))
+        f.pose = noise * f.pose if frame == "world" else f.pose * noise
 
 
 def dump_problem(prefix, out, graph, free_range, *, lam=1e-4, iters=2, tol=1e-12,
@@ -371,6 +373,12 @@ def synth_cfg(name):
                          image_size=(640, 480), intrinsics=Intrinsics(320.0, 320.0, 320.0, 240.0),
                          extent=n / 8.0)
         loops = n
+    elif name == "cfg4":
+        n = 4500
+        spec = SceneSpec(kind="square-loop", n_frames=n, seed=0, n_landmarks=72 * n,
+                         look="forward", image_size=(1226, 370),
+                         intrinsics=Intrinsics(718.856, 718.856, 607.193, 185.216), extent=440.0)
+        loops = n
     elif name == "mid":
         n = 120
         spec = SceneSpec(kind="circle", n_frames=n, seed=0, n_landmarks=max(1200, 12 * n) * 6,
@@ -390,14 +398,14 @@ def synth_cfg(name):
             tri.extend((old, k, recent) for k in range(32))
         graph.add_edges(tri, kind=LOOP)
     fill_flow(graph, scene, OracleConfig(pixel_noise_sigma=0.3), seed=1)
-    perturb_poses(graph, 0.02, seed=11)
+    perturb_poses(graph, 0.02, seed=11, frame="camera" if name == "cfg4" else "world")
     print(f"  {name}: {graph.n_frames} frames, {len(graph.edges)} edges, "
           f"{time.time() - t0:.1f}s")
     return spec, graph
 
 
-def case_synth(with_cfg3):
-    names = ["cfg1", "cfg2", "mid"] + (["cfg3"] if with_cfg3 else [])
+def case_synth(with_cfg3, names=None):
+    names = names or (["cfg1", "cfg2", "mid"] + (["cfg3"] if with_cfg3 else []))
     path = os.path.join(HERE, "synth_hashes.json")
     table = json.load(open(path)) if os.path.exists(path) else {}
     for name in names:
@@ -435,11 +443,13 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--synth-names", default=None, help="e.g. cfg4 (hash table entries to add)")
     args = ap.parse_args()
     cases = {"small": case_small, "window": case_window, "loops": case_loops,
              "edges": case_edges, "reproject": case_reproject, "cholesky": case_cholesky,
              "detect": case_detect, "fixture": case_fixture,
-             "synth": lambda: case_synth(args.with_cfg3)}
+             "synth": lambda: case_synth(args.with_cfg3, args.synth_names and
+                                         args.synth_names.split(","))}
     for name, fn in cases.items():
         if args.only and name not in args.only.split(","):
             continue

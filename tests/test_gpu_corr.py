@@ -88,3 +88,62 @@ def test_corr_on_reprojected_patches():
                     torch.zeros(40, dtype=torch.int32, device="cuda"))
     flat = out[:, 0].reshape(40, 9, 49).argmax(-1).cpu().numpy()
     assert np.all(flat == 24)
+
+
+def bench_shape_case(rng, E, H, W, F=24, P=4000, C=128):
+    """Edges at the bench feature shapes (cfg3 1/4-res 120x160, cfg4 KITTI
+    92x306), patch spreads as in a 3x3 patch reprojected at 1/4 resolution."""
+    g = (rng.normal(size=(P, 9, C)) / np.sqrt(C)).astype(np.float32)
+    f = (rng.normal(size=(F, H, W, C)) / np.sqrt(C)).astype(np.float32)
+    base = rng.uniform(-2, [W + 2, H + 2], size=(E, 1, 2))
+    offs = np.stack(np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0), -1).reshape(1, 9, 2)
+    coords = base + 0.25 * offs * rng.uniform(0.7, 1.4, size=(E, 1, 1))
+    ii = rng.integers(0, P, E).astype(np.int32)
+    jj = np.sort(rng.integers(0, F, E)).astype(np.int32)     # grouped by target frame
+    return g, f, coords, ii, jj
+
+
+@pytest.mark.parametrize("H,W", [(120, 160), (92, 306)])
+def test_corr_bench_shapes(H, W):
+    """Full bench-size launch (48k edges, both levels, C=128 bf16) checked on
+    a seeded sample of 1500 edges: (1) against the oracle on the same bf16
+    values (kernel arithmetic: |err| <= 2e-4), (2) against the oracle on the
+    ORIGINAL fp32 features -- the end-to-end error of storing features in
+    bf16, stated tolerance |err| <= 4e-3 absolute and RMS error <= 1% of
+    the output RMS (outputs ~ N(0, 0.09^2))."""
+    rng = np.random.default_rng(H * W)
+    E = 48_000
+    g, f, coords, ii, jj = bench_shape_case(rng, E, H, W)
+    gd = torch.as_tensor(g, device="cuda").bfloat16()
+    fd = torch.as_tensor(f, device="cuda").bfloat16()
+    pyr = corr.pyramid(fd)
+    out = corr.corr(gd, pyr, torch.as_tensor(coords, device="cuda"),
+                    torch.as_tensor(ii, device="cuda"), torch.as_tensor(jj, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    sel = np.sort(rng.choice(E, 1500, replace=False))
+    got = out.cpu().numpy()[sel]
+    ref_b = corr_oracle.corr(gd.double().cpu().numpy(),
+                             [fd.double().cpu().numpy(), pyr[1].double().cpu().numpy()],
+                             coords[sel], ii[sel], jj[sel])
+    assert np.abs(got - ref_b).max() < 2e-4
+    ref_f = corr_oracle.corr(g, [f, corr_oracle.avg_pool4(f)], coords[sel], ii[sel], jj[sel])
+    err = got - ref_f
+    assert np.abs(err).max() < 4e-3, np.abs(err).max()
+    assert np.sqrt((err ** 2).mean()) < 0.01 * np.sqrt((ref_f ** 2).mean())
+
+
+def test_corr_single_level_and_odd_counts():
+    """One pyramid level, edge counts that do not fill the last round of
+    items, C=64 (12-stage ring)."""
+    rng = np.random.default_rng(7)
+    for E in (1, 149, 1001):
+        g, f, coords, ii, jj = make(rng, E=E, C=64, F=3, H=28, W=36, P=40)
+        gd = torch.as_tensor(g, device="cuda").bfloat16()
+        fd = torch.as_tensor(f, device="cuda").bfloat16()
+        out = corr.corr(gd, [fd], torch.as_tensor(coords, device="cuda"),
+                        torch.as_tensor(ii, device="cuda"), torch.as_tensor(jj, device="cuda"))
+        ref = corr_oracle.corr(gd.double().cpu().numpy(), [fd.double().cpu().numpy()],
+                               coords, ii, jj)
+        assert out.shape == (E, 1, 9, 7, 7)
+        assert np.abs(out.cpu().numpy() - ref).max() < 2e-4

@@ -40,11 +40,12 @@ def test_inputs_bit_identical(name):
 
 
 @pytest.mark.slow
-def test_cfg3_inputs_bit_identical():
+@pytest.mark.parametrize("name", [n for n in ("cfg3", "cfg4") if n in TABLE])
+def test_large_inputs_bit_identical(name):
     if os.environ.get("DPV_SLOW") != "1":
-        pytest.skip("set DPV_SLOW=1 (cfg3 generation takes ~1 min)")
-    _, graph, _ = synthetic.make_config("cfg3")
-    ref = TABLE["cfg3"]
+        pytest.skip("set DPV_SLOW=1 (cfg3 / cfg4 generation takes ~0.5 / ~1.5 min)")
+    _, graph, _ = synthetic.make_config(name)
+    ref = TABLE[name]
     assert graph.n_edges == ref["n_edges"]
     got = digests(graph)
     assert {k: got[k] for k in ref["sha256"]} == ref["sha256"]
