@@ -72,6 +72,14 @@ def parse():
     return ap.parse_args()
 
 
+_T0 = time.perf_counter()
+
+
+def progress(msg):
+    """Phase marker on stderr (the JSON line stays the only stdout line)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -275,7 +283,7 @@ class Stepper:
             corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
             self.ev_join.record()
         if w["sharded"]:
-            w["prob"].allreduce_system()      # NCCL: reduced pose system
+            w["prob"].allreduce_system()      # one packed all-reduce
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
                 "solve")
         L.check(lib.dpv_apply_step(self.h, P(q), P(t), P(d), P(self.dp), P(self.dd), P(self.q2),
@@ -329,7 +337,7 @@ class Stepper:
             k1()
         L.check(lib.dpv_assemble_rest(self.h, P(t), s), "assemble_rest")
         if w["sharded"]:
-            w["prob"].allreduce_system()      # NCCL: the reduced pose system
+            w["prob"].allreduce_system()      # one packed all-reduce, no host sync
         if late:
             k1()
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
@@ -558,7 +566,9 @@ def run_ours(args):
         torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK))
+    progress("build workload")
     work = build_workload(args, torch)
+    progress("workload built")
     st = Stepper(work, torch)
     # device-resident step: one LM iteration with speculative assembly (the
     # native driver's flow); the sharded path keeps assemble + NCCL + objective
@@ -591,6 +601,7 @@ def run_ours(args):
             print(f"[bench] CUDA graph capture failed ({exc!r}); eager steps", file=sys.stderr)
             graph = None
             torch.cuda.synchronize()
+    progress("timed steps")
     launches0 = _lib.lib().dpv_launch_count()
     clk.mark_start()
     if graph is not None:
@@ -612,6 +623,7 @@ def run_ours(args):
     # per-kernel CUDA-event timing pass (separate, so the headline has no event overhead)
     # per-kernel CUDA-event pass: the correlation runs on the main stream here,
     # so every kernel is timed alone (the headline overlaps it with the BA)
+    progress("per-kernel timing pass")
     st.overlap = False
     _lib.timing_enable(True)
     for _ in range(args.steps):
@@ -659,7 +671,9 @@ def run_ours(args):
     # e2e through the C-ABI from pinned host buffers
     e2e = None
     if not args.no_e2e and world == 1:
+        progress("e2e")
         e2e = run_e2e_solve(work, args, torch)
+        progress("e2e per-iteration upload")
         # the stricter variant: every LM iteration re-uploads all targets
         e2e["per_iteration_upload"] = run_e2e(work, st, args, torch)
 
@@ -669,7 +683,9 @@ def run_ours(args):
     window1 = None
     batch = None
     if not args.no_global and world == 1:
+        progress("global BA")
         glob = run_global(work, args, torch)
+        progress("window steps")
         try:
             window = run_window(args, torch)
         except Exception as exc:     # reported, not fatal for the headline
@@ -679,6 +695,7 @@ def run_ours(args):
         except Exception as exc:
             window1 = {"error": repr(exc)}
         try:
+            progress("batch replicas")
             batch = None if args.no_batch else run_batch(args, torch, n_seq=args.batch_seqs)
         except Exception as exc:
             batch = {"error": repr(exc)}
@@ -690,7 +707,9 @@ def run_ours(args):
                 "lm_attempts": rep["attempts"], "final_objective": rep["final_objective"],
                 "includes": "native LM over the sharded system (index prebuilt)"}
 
+    progress("cpu baseline sample")
     cpu = None if (args.no_cpu or world > 1) else cpu_sample(work)
+    progress("done")
     if world > 1:
         tdist.destroy_process_group()
         if rank != 0:
@@ -722,8 +741,9 @@ def run_ours(args):
                             "all-reduce of the reduced pose system, redundant sparse solve, "
                             "retraction, edge pass at the candidate + all-reduce of its "
                             "objective; K1 beside it"),
-                   "parallelism": (f"edge-shard x{world} by depth row, NCCL all-reduce of the "
-                                   "reduced pose system" if world > 1 else "single GPU"),
+                   "parallelism": (f"edge-shard x{world} by depth row, one "
+                                   f"{args.dist_backend.upper()} all-reduce of the packed reduced "
+                                   "pose system per step" if world > 1 else "single GPU"),
                    "l2": f"inputs larger than L2 (flow targets {work['E'] * 144 / 1e9:.2f} GB, "
                          "126 MB L2)"},
         "gpu_launches": int(launches),
@@ -998,7 +1018,7 @@ def run_window(args, torch, reps=5, config="cfg2"):
             "includes": "index build, correlation, native LM, write-back (wall clock, synced)"}
 
 
-def run_batch(args, torch, n_seq=8, reps=5, threads=0):
+def run_batch(args, torch, n_seq=8, reps=5, threads=0, seed0=0, warm=2, sequential_too=True):
     """cfg5: n_seq independent TartanAir-shape sequences on
     this GPU as replicas.  One batch step = for every sequence a new 22-frame
     BAProblem, the correlation of its window edges (2 levels, bf16) and
@@ -1011,9 +1031,9 @@ def run_batch(args, torch, n_seq=8, reps=5, threads=0):
     C = args.channels
     fdt = torch.bfloat16 if args.feat_dtype == "bf16" else torch.float32
     for s in range(n_seq):
-        scene, graph, free = synthetic.make_config("cfg5", seed=s)
+        scene, graph, free = synthetic.make_config("cfg5", seed=seed0 + s)
         w, h = scene.spec.image_size
-        gen = torch.Generator(device="cuda").manual_seed(100 + s)
+        gen = torch.Generator(device="cuda").manual_seed(100 + seed0 + s)
         fmap = (torch.randn((graph.n_frames, h // 4, w // 4, C), generator=gen, device="cuda")
                 / math.sqrt(C)).to(fdt)
         gmap = (torch.randn((graph.n_patches, 9, C), generator=gen, device="cuda")
@@ -1080,28 +1100,85 @@ def run_batch(args, torch, n_seq=8, reps=5, threads=0):
     tb, ts = [], []
     E = 0
     out = []
-    for r in range(reps + 2):
+    for r in range(reps + warm):
         reset()
         t0 = time.perf_counter()
         E, out = batched()
-        if r >= 2:
+        if r >= warm:
             tb.append((time.perf_counter() - t0) * 1e3)
-        reset()
-        t0 = time.perf_counter()
-        sequential()
-        if r >= 2:
-            ts.append((time.perf_counter() - t0) * 1e3)
-    ms, ms_seq = float(np.median(tb)), float(np.median(ts))
+        if sequential_too:
+            reset()
+            t0 = time.perf_counter()
+            sequential()
+            if r >= warm:
+                ts.append((time.perf_counter() - t0) * 1e3)
+    ms = float(np.median(tb))
+    ms_seq = float(np.median(ts)) if ts else float("nan")
     bad = [type(x).__name__ for x in out if isinstance(x, Exception)]
     return {"config": "cfg5: " + synthetic.DESCRIPTIONS["cfg5"], "sequences": n_seq,
             "E_total": E, "ms_per_batch": ms, "window_steps_per_s": n_seq / (ms * 1e-3),
             "value": 2 * E / (ms * 1e-3), "unit": "patch-edges/s (x2 LM iters)",
             "sequential_ms": ms_seq, "batching_gain": ms_seq / ms,
-            "phase_ms": {k: float(np.median(v[2:])) for k, v in phases.items()},
+            "phase_ms": {k: float(np.median(v[warm:])) for k, v in phases.items()},
+            "timed_ms": tb,
             "iterations": [x.iterations for x in out if not isinstance(x, Exception)],
             "failed": bad,
             "includes": "index build, correlation, native LM, write-back for every sequence "
                         "(wall clock, synced); replicas on one stream + host worker each"}
+
+
+def run_replicas(args):
+    """cfg5 across GPUs (replicas only, no collective on the data
+    path): rank r solves sequences r*B .. r*B+B-1 (B = --batch-seqs) as one
+    concurrent batch per step (index build + correlation + 2 LM iterations
+    per sequence, see run_batch).  Steps are bracketed by a barrier and a
+    device synchronisation; the step time is the max over ranks and `value`
+    counts every rank's patch-edges x LM iterations."""
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    tdist = None
+    if world > 1:
+        import torch.distributed as tdist
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(args.dist_backend)
+        tdist.barrier()
+    from paper_2408_01654_b200 import _lib
+    B = args.batch_seqs
+    l0 = _lib.lib().dpv_launch_count()
+    res = run_batch(args, torch, n_seq=B, reps=args.steps, seed0=rank * B,
+                    warm=max(args.warmup, 3), sequential_too=False)
+    launches = (_lib.lib().dpv_launch_count() - l0) * args.steps // (args.steps + max(args.warmup, 3))
+    ms = float(np.mean(res["timed_ms"]))
+    units = 2.0 * res["E_total"]
+    if world > 1:
+        t = torch.tensor([ms, units], dtype=torch.float64, device="cuda")
+        mx = t[:1].clone()
+        tdist.all_reduce(mx, op=tdist.ReduceOp.MAX)
+        tot = t[1:].clone()
+        tdist.all_reduce(tot)
+        ms, units = float(mx.item()), float(tot.item())
+        tdist.barrier()
+        tdist.destroy_process_group()
+        if rank != 0:
+            return None
+    return {
+        "metric": "patch-edges/sec for corr lookup + Gauss-Newton BA step; global loop-closure BA ms",
+        "value": units / (ms * 1e-3), "unit": "patch-edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator restated bit-exactly; random features)",
+        "config": {"workload": f"cfg5: {B} TartanAir-shape sequences per GPU, one 22-frame window "
+                               "step each (index build + corr + 2 LM iterations), replicas",
+                   "sequences": B * world, "parallelism": f"replicas x{world} (no collective)",
+                   "l2": "per-step index rebuild and fresh problems (inputs re-read from HBM)"},
+        "gpu_launches": int(launches),
+        "batch": {k: v for k, v in res.items() if k != "timed_ms"},
+    }
 
 
 def run_global(work, args, torch):
@@ -1182,6 +1259,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         line = run_reference(args)
+    elif args.config == "cfg5":
+        line = run_replicas(args)
     else:
         line = run_ours(args)
     rank = int(os.environ.get("RANK", "0"))

@@ -550,11 +550,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
                 for (int a = 0; a < 3; ++a)
                     ew[3 * h + a] = Rj[3 * a] * ep[3 * h] + Rj[3 * a + 1] * ep[3 * h + 1] +
                                     Rj[3 * a + 2] * ep[3 * h + 2];
-            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 8);
+            double2* et = reinterpret_cast<double2*>(e_terms + (int64_t)e * 6);
             et[0] = make_double2(ew[0], ew[1]);
             et[1] = make_double2(ew[2], ew[3]);
             et[2] = make_double2(ew[4], ew[5]);
-            et[3] = make_double2(cdd, gd);
+            reinterpret_cast<double2*>(e_terms + 6 * E)[e] = make_double2(cdd, gd);
         }
         if (cur.e1 == cur.se1) {          // segment done: reduce, rotate, write
             const int64_t sg = cur.s;
@@ -613,6 +613,9 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
                        const double* e_terms, double* depth_diag, double* rhs_depth,
                        uint8_t* active, double* cinv0, unsigned long long* grad_bits,
                        unsigned long long* n_inactive) {
+    // (c_dd, g_d) of edge e: the SoA tail of e_terms, 16 B per edge, so the
+    // adjacent rows' edges of one segment share sectors
+    const double2* e_cg = reinterpret_cast<const double2*>(e_terms + 6 * E);
     double gmax = 0.0;
     unsigned long long inact = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P;
@@ -622,16 +625,15 @@ __global__ void k_rows(int64_t P, int64_t E, const int32_t* row_ptr, const int32
         int32_t k = row_ptr[r];
         for (; k + 1 < k1; k += 2) {       // two gathers in flight, same order
             const int32_t ea = __ldg(row_pos + k), eb = __ldg(row_pos + k + 1);
-            const double2 ca = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)ea * 8 + 6));
-            const double2 cb = __ldg(reinterpret_cast<const double2*>(e_terms + (int64_t)eb * 8 + 6));
+            const double2 ca = __ldg(e_cg + ea);
+            const double2 cb = __ldg(e_cg + eb);
             c += ca.x;
             g += ca.y;
             c += cb.x;
             g += cb.y;
         }
         if (k < k1) {
-            const double2 cg = __ldg(reinterpret_cast<const double2*>(
-                e_terms + (int64_t)__ldg(row_pos + k) * 8 + 6));
+            const double2 cg = __ldg(e_cg + __ldg(row_pos + k));
             c += cg.x;
             g += cg.y;
         }
@@ -674,8 +676,8 @@ __global__ void __launch_bounds__(256) k_incidences2(int64_t I, const int32_t* _
         int32_t k = k0;
         for (; k + 1 < k1; k += 2) {
             const int32_t ca = __ldg(inc_con + k), cb = __ldg(inc_con + k + 1);
-            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 8);
-            const double2* eb = reinterpret_cast<const double2*>(e_terms + (int64_t)(cb >> 1) * 8);
+            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 6);
+            const double2* eb = reinterpret_cast<const double2*>(e_terms + (int64_t)(cb >> 1) * 6);
             double2 va[3], vb[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -696,7 +698,7 @@ __global__ void __launch_bounds__(256) k_incidences2(int64_t I, const int32_t* _
         }
         if (k < k1) {
             const int32_t ca = __ldg(inc_con + k);
-            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 8);
+            const double2* ea = reinterpret_cast<const double2*>(e_terms + (int64_t)(ca >> 1) * 6);
             const double sa = (ca & 1) ? -1.0 : 1.0;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(256) k_incidences2(int64_t I, const int32_t* _
 
 // small problems (few rows): one warp per row, lanes over the row's edges,
 // xor-tree reduction (fixed order)
-__global__ void k_rows_warp(int64_t P, const int32_t* row_ptr, const int32_t* row_pos,
+__global__ void k_rows_warp(int64_t P, int64_t E, const int32_t* row_ptr, const int32_t* row_pos,
                             const double* e_terms, double* depth_diag, double* rhs_depth,
                             uint8_t* active, double* cinv0, unsigned long long* grad_bits,
                             unsigned long long* n_inactive) {
@@ -730,8 +732,8 @@ __global__ void k_rows_warp(int64_t P, const int32_t* row_ptr, const int32_t* ro
     for (int64_t r = warp; r < P; r += nwarps) {
         double c = 0.0, g = 0.0;
         for (int32_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) {
-            const double2 cg = __ldg(reinterpret_cast<const double2*>(
-                e_terms + (int64_t)__ldg(row_pos + k) * 8 + 6));
+            const double2 cg = __ldg(reinterpret_cast<const double2*>(e_terms + 6 * E) +
+                                     __ldg(row_pos + k));
             c += cg.x;
             g += cg.y;
         }
@@ -1197,7 +1199,7 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
         DPV_TSTART("rows", st);
         if (p->P < (int64_t)sm_count() * 64)      // few rows: a warp each
             k_rows_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
-                p->P, p->row_ptr, p->row_pos, p->e_terms, p->depth_diag, p->rhs_depth,
+                p->P, p->E, p->row_ptr, p->row_pos, p->e_terms, p->depth_diag, p->rhs_depth,
                 p->active, p->cinv0, grad_bits, n_inactive);
         else
             k_rows<<<grid_for(p->P, 256), 256, 0, st>>>(p->P, p->E, p->row_ptr, p->row_pos,

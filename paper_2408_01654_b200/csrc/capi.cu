@@ -224,6 +224,7 @@ bool lookup(const dpv_problem* p, const char* name, ArrayDesc& a) {
         {"rhs_pose", p->rhs_pose, p->n * 6, 0},
         {"rhs_schur", p->rhs_schur, p->n * 6, 0},
         {"scal", p->scal, 16, 0},
+        {"sysbuf", p->sysbuf, p->sysbuf ? 2 * p->W * 36 + 2 * p->n * 6 + dpv::kRedTail : 0, 0},
         {"dense", p->dense, p->dense ? (N + 1) * p->dense_ld : 0, 0},
     };
     for (const Entry& e : table) {

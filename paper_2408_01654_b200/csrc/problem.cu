@@ -1258,10 +1258,16 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     DPV_TRY(P->alloc(&P->cinv0, NPD));
     DPV_TRY(P->alloc(&P->inc_block, I * 6));
     DPV_TRY(P->alloc(&P->uinc, I * 6));
-    DPV_TRY(P->alloc(&P->pose_blocks, W * 36));
-    DPV_TRY(P->alloc(&P->schur_blocks, W * 36));
-    DPV_TRY(P->alloc(&P->rhs_pose, P->n * 6));
-    DPV_TRY(P->alloc(&P->rhs_schur, P->n * 6));
+    // [pose_blocks | schur_blocks | rhs_pose | rhs_schur | reduction tail]
+    // in ONE allocation: the sharded BA sums the whole pose system over the
+    // ranks with a single all-reduce; the tail carries one
+    // depth-gradient slot per rank (max folded into the sum)
+    DPV_TRY(P->alloc(&P->sysbuf, 2 * W * 36 + 2 * P->n * 6 + dpv::kRedTail));
+    P->pose_blocks = P->sysbuf;
+    P->schur_blocks = P->pose_blocks + W * 36;
+    P->rhs_pose = P->schur_blocks + W * 36;
+    P->rhs_schur = P->rhs_pose + P->n * 6;
+    P->red_tail = P->rhs_schur + P->n * 6;
     DPV_TRY(P->alloc(&P->scal, 16));
     DPV_TRY(P->alloc(&P->obj_part, kObjBlocks));
     DPV_TRY(P->alloc(&P->red_rhs, P->n * 6 + 8));

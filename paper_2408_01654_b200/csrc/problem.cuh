@@ -136,7 +136,7 @@ struct dpv_problem {
 
     // ---- assembled system -----------------------------------------------------
     double* frame_R = nullptr;     // (F, 9)
-    double* e_terms = nullptr;     // (E, 8): e_pd[6], c_dd, g_d
+    double* e_terms = nullptr;     // [e_pd (E, 6) | (c_dd, g_d) (E, 2)]
     double* seg_h = nullptr;       // (S, 21) upper-triangular sum of J^T W J
     double* seg_g = nullptr;       // (S, 6)  sum of J^T W r
     double* seg_obj = nullptr;     // (S) sum of w r^2 (LM candidate objective)
@@ -146,6 +146,8 @@ struct dpv_problem {
     double* cinv0 = nullptr;       // (P)
     double* inc_block = nullptr;   // (I, 6)
     double* uinc = nullptr;        // (I, 6) inc_block * cinv0[row]
+    double* sysbuf = nullptr;      // one allocation: the four arrays below + red_tail
+    double* red_tail = nullptr;    // (kRedTail) per-rank depth-gradient slots
     double* pose_blocks = nullptr; // (W, 36)
     double* schur_blocks = nullptr;// (W, 36)
     double* rhs_pose = nullptr;    // (n, 6)
@@ -213,6 +215,7 @@ struct dpv_problem {
 
 namespace dpv {
 constexpr int kSegMax = 128;      // edges per segment chunk
+constexpr int kRedTail = 64;      // ranks whose depth gradient rides in the packed all-reduce
 constexpr int kSyrkMaxRows = 128;            // rows per grouped-Schur chunk
 constexpr int kSyrkSmemDoubles = 12800;      // 100 KB of W_g staging per chunk (2 CTAs/SM)
 int32_t configure_pool();

@@ -4,15 +4,19 @@ One process per GPU.  The edge list of the global loop-closure BA is
 partitioned by depth row (source patch), so each depth row's incidences,
 Schur pairs and back-substitution stay on one shard.  Per LM iteration:
 
-1. every rank assembles its shard (K2+K3+K4a) on the *global* block pattern
-   (``dpv_problem_create_ex`` merges the global union keys into the shard);
-2. one all-reduce (sum, float64) of [pose_blocks | schur_blocks | rhs_pose |
-   rhs_schur] -- the reduced pose system -- plus an all-reduce(max) of the
-   depth gradient norm;
-3. every rank forms S(lambda) and factorises it redundantly (deterministic,
+1. rank 0 builds the (state-independent) full index once and broadcasts the
+   global block pattern (union keys) and gauge; every rank indexes only its
+   shard, aligned to that pattern (``dpv_problem_create_ex``);
+2. every rank assembles its shard (K2+K3+K4a);
+3. ONE all-reduce (sum, float64) of the packed buffer [pose_blocks |
+   schur_blocks | rhs_pose | rhs_schur | per-rank depth-gradient slots] -- the
+   reduced pose system and, folded into the same sum, each rank's depth
+   gradient max; no host synchronisation;
+4. every rank forms S(lambda) and factorises it redundantly (deterministic,
    so all ranks hold the identical pose update), back-substitutes its own
    depth rows and evaluates its share of the candidate objective;
-4. one all-reduce(sum) of the candidate objective per damping attempt.
+5. one all-reduce(sum) of the candidate objective per damping attempt, read
+   back together with the solve status and the gradient (one host read).
 
 The LM logic is ba.solve (ba.py:534-605) verbatim in control flow.  The host
 side (partitioning, reductions) runs on CPU with the gloo backend in the tests;
@@ -60,6 +64,23 @@ def shard_rows(graph, free_range, world: int):
     return out, bounds
 
 
+def allreduce_packed(sysvec, tail, rhs_pose, depth_g, rank, world, dist, group=None):
+    """ONE all-reduce (sum) of the packed [pose_blocks | schur_blocks |
+    rhs_pose | rhs_schur | tail] buffer.  Every rank writes its depth-gradient
+    max into its own tail slot (the others zero), so the sum carries every
+    rank's value and the max (ba.py:431 gradient_norm) is taken locally:
+    max(|rhs_pose|_inf of the summed system, max over the slots).  Returns a
+    0-d tensor on the buffer's device (no host read)."""
+    import torch
+    tail.zero_()
+    tail[rank:rank + 1].copy_(depth_g.reshape(1))
+    dist.all_reduce(sysvec, group=group)
+    g = tail[:world].max()
+    if rhs_pose.numel():
+        g = torch.maximum(g, rhs_pose.abs().max())
+    return g
+
+
 class ShardedProblem:
     """This rank's shard of the global BA, aligned to the global block pattern."""
 
@@ -75,15 +96,27 @@ class ShardedProblem:
         self.free_range = tuple(free_range)
         shards, _ = shard_rows(graph, free_range, self.world)
         self.edge_indices = shards[self.rank]
-        # the global pattern and gauge from the full index (cheap on the GPU)
-        full = BAProblem(graph, free_range)
-        full._ensure()
-        ukeys = full.view("union_keys").clone()
-        info = full._info
-        self.scale_degenerate = int(info.scale_degenerate)
-        self.touched0 = int(info.touched_fixed0)
-        self.n_edges_total = int(info.n_edges)
-        del full
+        # the global block pattern and gauge: rank 0 builds the full index
+        # (state-independent, once per problem) and broadcasts the union keys
+        # plus three scalars; the other ranks only ever index their shard
+        dev = torch.device("cuda", torch.cuda.current_device())
+        meta = torch.zeros(4, dtype=torch.int64, device=dev)
+        if self.rank == 0:
+            full = BAProblem(graph, free_range)
+            full._ensure()
+            ukeys = full.view("union_keys").clone()
+            info = full._info
+            meta[0] = len(ukeys)
+            meta[1] = int(info.scale_degenerate)
+            meta[2] = int(info.touched_fixed0)
+            meta[3] = int(info.n_edges)
+            del full
+        dist.broadcast(meta, 0, group=group)
+        n_keys, self.scale_degenerate, self.touched0, self.n_edges_total = (int(x) for x in
+                                                                             meta.tolist())
+        if self.rank != 0:
+            ukeys = torch.empty(n_keys, dtype=torch.int64, device=dev)
+        dist.broadcast(ukeys, 0, group=group)
         lib = _lib.lib()
         mir = graph.device()
         g = _lib.DpvGraph()
@@ -113,8 +146,14 @@ class ShardedProblem:
         self.n = int(info.n_free)
         self.P = int(info.n_depths)
         views = {k: _lib.device_view(h, k, self) for k in
-                 ("pose_blocks", "schur_blocks", "rhs_pose", "rhs_schur", "scal", "depth_patch")}
+                 ("pose_blocks", "schur_blocks", "rhs_pose", "rhs_schur", "scal", "depth_patch",
+                  "sysbuf")}
         self.views = views
+        n_sys = 2 * len(ukeys) * 36 + 2 * self.n * 6
+        # the packed pose system: ONE all-reduce per LM iteration
+        self.sysvec = views["sysbuf"]
+        self.red_tail = self.sysvec[n_sys:]
+        assert self.world <= self.red_tail.numel(), "more ranks than depth-gradient slots"
 
     # BAProblem-like accessors used by bench.py's stepper
     damping = 1e-4
@@ -146,17 +185,13 @@ class ShardedProblem:
         return mir["q"].clone(), mir["t"].clone(), d
 
     def allreduce_system(self):
-        """Sum the reduced pose system over ranks; returns the global gradient norm."""
+        """Sum the reduced pose system over the ranks (allreduce_packed on
+        the handle's packed buffer); returns the global gradient norm as a
+        DEVICE scalar, so the step needs no host synchronisation."""
         import torch
-        v = self.views
-        for k in ("pose_blocks", "schur_blocks", "rhs_pose", "rhs_schur"):
-            self.dist.all_reduce(v[k], group=self.group)
-        scal = v["scal"]
-        depth_g = scal[7:8].view(torch.int64).view(torch.float64).clone()
-        self.dist.all_reduce(depth_g, op=self.dist.ReduceOp.MAX, group=self.group)
-        pose_g = v["rhs_pose"].abs().max() if self.n else torch.zeros((), dtype=torch.float64,
-                                                                     device="cuda")
-        return max(float(pose_g), float(depth_g))
+        depth_g = self.views["scal"][7:8].view(torch.int64).view(torch.float64)
+        return allreduce_packed(self.sysvec, self.red_tail, self.views["rhs_pose"], depth_g,
+                                self.rank, self.world, self.dist, self.group)
 
     def objective(self, q, t, d, out):
         _lib.check(_lib.lib().dpv_objective(self.h, _lib.ptr(q), _lib.ptr(t), _lib.ptr(d),
@@ -183,16 +218,19 @@ class ShardedProblem:
         for _ in range(max_iterations):
             tic = time.perf_counter()
             _lib.check(lib.dpv_assemble(self.h, P(q), P(t), P(d), s()), "assemble")
-            grad = self.allreduce_system()
-            rep["gradient_norm"] = grad
+            grad_t = self.allreduce_system()
             accepted = solved = singular = False
             for _ in range(LM_MAX_ESCALATIONS + 1):
                 rep["attempts"] += 1
                 _lib.check(lib.dpv_solve(self.h, lam, P(dp), P(dd), P(st), s()), "solve")
                 _lib.check(lib.dpv_apply_step(self.h, P(q), P(t), P(d), P(dp), P(dd), P(q2), P(t2),
                                               P(d2), s()), "apply_step")
-                cand = float(self.objective(q2, t2, d2, obj_t).item())
-                if int(st[0].item()) != 0:
+                self.objective(q2, t2, d2, obj_t)
+                # one host read per damping attempt: candidate, status, gradient
+                host = torch.stack([obj_t[0], st[0].to(torch.float64), grad_t]).cpu()
+                cand, grad = float(host[0]), float(host[2])
+                rep["gradient_norm"] = grad
+                if int(host[1]) != 0:
                     singular = True
                     lam *= LM_LAMBDA_GROW
                     if lam > LM_LAMBDA_MAX:

@@ -13,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2408_01654_b200 import synthetic
-from paper_2408_01654_b200.dist import shard_rows
+from paper_2408_01654_b200.dist import allreduce_packed, shard_rows
 
 
 def small_graph():
@@ -75,9 +75,16 @@ def _worker(rank, world, port, out):
     schur = np.zeros((len(union), 6, 6))
     pose[where] = sysm.pose_blocks
     schur[where] = sysm.schur_blocks
+    # the packed buffer of dist.allreduce_packed: ONE all-reduce carries the
+    # pose system and every rank's depth-gradient max (one slot per rank)
     buf = torch.from_numpy(np.concatenate([pose.ravel(), schur.ravel(), sysm.rhs_pose.ravel(),
-                                           sysm.rhs_schur.ravel()]))
-    dist.all_reduce(buf)
+                                           sysm.rhs_schur.ravel(), np.full(8, np.nan)]))
+    n_sys = buf.numel() - 8
+    depth_g = np.abs(sysm.rhs_depth[sysm.active]).max() if sysm.active.any() else 0.0
+    grad = allreduce_packed(buf, buf[n_sys:], buf[2 * len(union) * 36:2 * len(union) * 36
+                                                  + 6 * full.n_free],
+                            torch.tensor(depth_g, dtype=torch.float64), rank, world, dist)
+    buf = buf[:n_sys]
     obj = torch.tensor([O.objective(prob)], dtype=torch.float64)
     dist.all_reduce(obj)
     if rank == 0:
@@ -94,6 +101,7 @@ def _worker(rank, world, port, out):
         out["rhs_schur"] = np.abs(got[2 * W * 36 + n6:] - ref.rhs_schur.ravel()).max() / max(
             1.0, np.abs(ref.rhs_schur).max())
         out["obj"] = abs(obj.item() - O.objective(full)) / O.objective(full)
+        out["grad"] = abs(float(grad) - ref.gradient_norm) / ref.gradient_norm
     dist.destroy_process_group()
 
 
