@@ -1255,6 +1255,10 @@ def run_reference(args):
 
 
 def main():
+    import faulthandler
+    # a stuck phase dumps every thread's stack to stderr (diagnostics only)
+    faulthandler.dump_traceback_later(int(os.environ.get("DPV_BENCH_WATCHDOG_S", "420")),
+                                      repeat=True, file=sys.stderr)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":

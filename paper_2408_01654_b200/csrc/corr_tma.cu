@@ -33,7 +33,6 @@ constexpr int kHalfBytes = kTapsPad * 128;   // one 64-channel half of the windo
 constexpr int kGHalfBytes = 16 * 128;     // 16 feature rows x 64 channels
 constexpr int kStages = 3;
 constexpr int kConsumers = 128;
-constexpr int kProducerWarp = 4;
 
 struct CellMeta {
     int ox, oy;        // cell tap-grid origin inside the window (x0 - r - bx0, y0 - r - by0)
@@ -125,15 +124,32 @@ __device__ __forceinline__ void split(double v, int& i0, float& fr) {
 
 // Per-NH (C / 64 channel halves) pipeline shape: stage bytes (window halves,
 // patch-feature halves, item metadata; 1024-aligned for the 128B swizzle),
-// NS stages in the ring, NG consumer groups of 4 warps (each group works on
-// its own item, so NG items are in flight per SM besides the prefetched ones).
+// NS stages in the ring, NP producer warps and NG consumer groups of 4 warps.
+// Both NP and NG divide NS, so every stage has ONE producer and ONE consumer
+// group, each walking that stage's items in order: an mbarrier parity wait
+// can then never alias a phase two completions away (with several producers
+// and a group count that does not divide NS, a group could pass its `full`
+// wait on a stage whose previous item had not been produced yet).
+#ifndef DPV_CORR_SMEM_KB
+#define DPV_CORR_SMEM_KB 200      // stage-ring budget per CTA
+#endif
+#ifndef DPV_CORR_CTAS
+#define DPV_CORR_CTAS 1           // CTAs per SM
+#endif
 template <int NH>
 struct CorrCfg {
     static constexpr int SB =
         ((NH * (kHalfBytes + kGHalfBytes) + (int)sizeof(ItemMeta) + 1023) / 1024) * 1024;
-    static constexpr int NS = (200 * 1024) / SB < 8 ? (200 * 1024) / SB : 8;
-    static constexpr int NG = NS - 1 < 4 ? NS - 1 : 4;
-    static constexpr int kThreadsT = 32 + NG * kConsumers;
+    static constexpr int NS0 = (DPV_CORR_SMEM_KB * 1024) / SB;
+    // C <= 128: 6 stages, 3 producers (one per pair of stages: a single
+    // producer warp, ~400 dependent scalar instructions per item, capped the
+    // kernel at ~1 item/us/SM), 3 consumer groups; C = 256: 3 stages, 1
+    // producer, 3 groups
+    static constexpr int NS = NS0 >= 6 ? 6 : (NS0 >= 3 ? 3 : (NS0 >= 1 ? NS0 : 1));
+    static constexpr int NP = NS == 6 ? 3 : 1;
+    static constexpr int NG = NS >= 3 ? 3 : NS;
+    static_assert(NS % NP == 0 && NS % NG == 0, "producers and groups must divide the stages");
+    static constexpr int kThreadsT = 32 * NP + NG * kConsumers;
     static constexpr size_t kSmem =
         (size_t)NS * SB + sizeof(float) * NG * kCellsT * kTapsPad + 1024;
 };
@@ -143,11 +159,11 @@ __device__ __forceinline__ void bar_group(int g) {
 }
 
 // One persistent CTA per SM; items are (edge, level) pairs, level fastest, so
-// both pyramid levels run in ONE launch.  Warp 0 is the TMA producer, warps
-// 1.. form NG consumer groups; local item k goes to stage k % NS and group
-// k % NG.
+// both pyramid levels run in ONE launch.  Warps 0..NP-1 are TMA producers,
+// the rest form NG consumer groups of 4 warps; local item k goes to stage
+// k % NS, producer k % NP and consumer group k % NG (= stage % NP / % NG).
 template <int NH>
-__global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, 1) k_corr_tma(
+__global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_tma(
     const __grid_constant__ CUtensorMap fmap0_map, const __grid_constant__ CUtensorMap fmap1_map,
     const __grid_constant__ CUtensorMap gmap_map, const __nv_bfloat16* __restrict__ fmap0,
     const __nv_bfloat16* __restrict__ fmap1, const __nv_bfloat16* __restrict__ gmap,
@@ -175,32 +191,47 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, 1) k_corr_tma(
     const int64_t n_my = NV > blockIdx.x ? (NV - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     constexpr int radius = 3, D = 8, O = 7;
 
-    if (warp == 0) {
-        // ---------------- producer ----------------
-        // the next item's coordinates and indices are loaded one item ahead
-        double cxn = 0.0, cyn = 0.0;
-        int32_t iin = 0, jjn = 0;
-        auto fetch = [&](int64_t u) {
-            if (u >= n_my) return;
-            const int64_t e = (blockIdx.x + u * (int64_t)gridDim.x) / levels;
-            if (lane < kCellsT) {
-                cxn = __ldg(coords + (e * kCellsT + lane) * 2);
-                cyn = __ldg(coords + (e * kCellsT + lane) * 2 + 1);
-            }
-            if (lane == 0) {
-                iin = __ldg(ii + e);
-                jjn = __ldg(jj + e);
+    constexpr int NP = Cfg::NP;
+    if (warp < NP) {
+        // ---------------- producers ----------------
+        // Producer warp p issues local items u = p, p + NP, ... into stages
+        // u % NS (NP divides NS: stage s belongs to producer s % NP).  Per item
+        // the producer does ~400 dependent scalar instructions (coordinate
+        // split, window origin, metadata, TMA issue) at ~5 cycles each, so a
+        // single producer warp per SM capped the kernel at ~1 item/us/SM.
+        // K2 coordinates and indices run kLook items ahead: lane group
+        // lg = lane / 9 (cells lc = lane % 9) holds the producer's i-th item
+        // with i % kLook == lg, loaded kLook iterations before it is used.
+        constexpr int kLook = 3;
+        const int lg = lane / kCellsT, lc = lane % kCellsT;
+        const int64_t n_mine = n_my > warp ? (n_my - warp + NP - 1) / NP : 0;
+        double cxr = 0.0, cyr = 0.0;
+        int32_t iir = 0, jjr = 0;
+        auto edge_of = [&](int64_t v) { return levels == 2 ? (v >> 1) : v; };
+        auto fetch = [&](int64_t i) {
+            if (i >= n_mine || lg != (int)(i % kLook)) return;
+            const int64_t e = edge_of(blockIdx.x + (warp + i * NP) * (int64_t)gridDim.x);
+            cxr = __ldg(coords + (e * kCellsT + lc) * 2);
+            cyr = __ldg(coords + (e * kCellsT + lc) * 2 + 1);
+            if (lc == 0) {
+                iir = __ldg(ii + e);
+                jjr = __ldg(jj + e);
             }
         };
-        fetch(0);
-        for (int64_t u = 0; u < n_my; ++u) {
+#pragma unroll
+        for (int q = 0; q < kLook; ++q) fetch(q);
+        for (int64_t i = 0; i < n_mine; ++i) {
+            const int64_t u = warp + i * NP;
             const int64_t v = blockIdx.x + u * (int64_t)gridDim.x;
-            const int64_t e = v / levels;
-            const int level = (int)(v - e * levels);
+            const int64_t e = edge_of(v);
+            const int level = levels == 2 ? (int)(v & 1) : 0;
             const int s = (int)(u % NS);
-            const double cx = cxn, cy = cyn;
-            const int32_t iic = iin, jjc = jjn;
-            fetch(u + 1);
+            const int src = (int)(i % kLook) * kCellsT;
+            const double cx = __shfl_sync(0xffffffffu, cxr, src + (lane < kCellsT ? lane : 0));
+            const double cy = __shfl_sync(0xffffffffu, cyr, src + (lane < kCellsT ? lane : 0));
+            const int32_t iic = __shfl_sync(0xffffffffu, iir, src);
+            const int32_t jjc = __shfl_sync(0xffffffffu, jjr, src);
+            fetch(i + kLook);
             mbar_wait(&empty[s], (unsigned)(((u / NS) & 1) ^ 1));
             ItemMeta* M = reinterpret_cast<ItemMeta*>(sm + s * SB + NH * (kHalfBytes + kGHalfBytes));
             const double scale = level == 0 ? 1.0 : 0.25;
@@ -253,7 +284,8 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, 1) k_corr_tma(
         return;
     }
     // ---------------- consumer groups (4 warps each) ----------------
-    const int grp = (warp - 1) >> 2, gw = (warp - 1) & 3, gtid = tid - 32 - grp * kConsumers;
+    const int grp = (warp - NP) >> 2, gw = (warp - NP) & 3,
+              gtid = tid - 32 * NP - grp * kConsumers;
     float* S = reinterpret_cast<float*>(sm + NS * SB) + grp * (kCellsT * kTapsPad);
     const int g = lane >> 2, t4 = lane & 3;
     // ldmatrix lane roles (128B swizzle: chunk' = chunk ^ (row % 8), rows of
@@ -419,7 +451,8 @@ int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap0, const v
         static size_t cur[3] = {0, 0, 0};
         DPV_TRY(ensure_smem(kern, smem, cur[slot]));
         const int64_t items = E * levels;
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, sm_count()));
+        const int grid =
+            (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sm_count() * DPV_CORR_CTAS));
         DPV_TSTART("corr", st);
         kern<<<grid, threads, smem, st>>>(fm[0], fm[1], gm,
                                           reinterpret_cast<const __nv_bfloat16*>(fmap0),
