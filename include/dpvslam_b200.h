@@ -266,6 +266,41 @@ int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev,
 int32_t dpv_block_fill_count(const int64_t* keys, int64_t n_keys, int64_t n, int64_t* count);
 
 /* ------------------------------------------------------------------------
+ * Sim(3) pose-graph optimisation (posegraph.py:121-196, optimize; SURVEY
+ * 8(f) rank 4).  Similarities as 8 doubles [tx ty tz qx qy qz qw s]
+ * (x -> s R x + t; the g2o field order, posegraph.py:12-14).  Constraint c:
+ * nodes (a_c, b_c) and constant M_c, residual r = log(M S_a^-1 S_b) in the
+ * tangent (rho, phi, sigma) (posegraph.py:91-104).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    double initial_objective;
+    double final_objective;
+    double max_residual_norm;    /* of the last linearisation */
+    double final_damping;
+} dpv_pgo_report;
+
+/* optimize(): Levenberg-Marquardt over node tangents, node 0 the gauge.
+ * nodes (n_nodes, 8) DEVICE, overwritten by the solution; ca_h / cb_h HOST
+ * and ca / cb DEVICE copies of the constraint node indices (int32, the host
+ * copy builds the block pattern); cm (n_cons, 8) DEVICE.  DPV_SINGULAR when
+ * the damped normal equations stay singular (SingularSystem). */
+int32_t dpv_pgo_optimize(int64_t n_nodes, double* nodes, int64_t n_cons, const int32_t* ca_h,
+                         const int32_t* cb_h, const int32_t* ca, const int32_t* cb,
+                         const double* cm, int32_t max_iterations, double tolerance,
+                         double damping, dpv_pgo_report* report, void* stream);
+/* residual_and_jacobian / objective (posegraph.py:91-104): r (n_cons, 7),
+ * J (n_cons, 7, 7) d r / d (left tangent of S_b) or NULL, objective (device
+ * scalar, sum r.r) or NULL.  All DEVICE. */
+int32_t dpv_pgo_linearize(int64_t n_nodes, const double* nodes, int64_t n_cons,
+                          const int32_t* ca, const int32_t* cb, const double* cm, double* r,
+                          double* J, double* objective, void* stream);
+/* sim3_exp / sim3_log (geometry.py:303-321), n items, DEVICE arrays. */
+int32_t dpv_sim3_exp(int64_t n, const double* tangents, double* sims, void* stream);
+int32_t dpv_sim3_log(int64_t n, const double* sims, double* tangents, void* stream);
+
+/* ------------------------------------------------------------------------
  * K1: per-edge correlation lookup (Eq. 4; no reference code).
  *   gmap  (n_src_patches, p*p, C)       patch features, channels-last
  *   fmap_l (n_frames, H_l, W_l, C)      level-l frame features, channels-last

@@ -47,6 +47,12 @@ class DpvLmParams(C.Structure):
                 ("lambda0", C.c_double)]
 
 
+class DpvPgoReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
+                ("initial_objective", C.c_double), ("final_objective", C.c_double),
+                ("max_residual_norm", C.c_double), ("final_damping", C.c_double)]
+
+
 class DpvLmReport(C.Structure):
     _fields_ = [
         ("iterations", C.c_int32), ("converged", C.c_int32),
@@ -89,6 +95,11 @@ SIGNATURES = {
     "dpv_problem_create_batch": (C.c_int32, [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp]),
     "dpv_lm_solve_batch": (C.c_int32, [C.c_int32, vp, vp, vp, vp, vp, vp, vp, C.c_int32, vp]),
     "dpv_cholesky_solve": (C.c_int32, [vp, vp, C.c_int64, vp, vp]),
+    "dpv_pgo_optimize": (C.c_int32, [C.c_int64, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int32,
+                                     C.c_double, C.c_double, C.POINTER(DpvPgoReport), vp]),
+    "dpv_pgo_linearize": (C.c_int32, [C.c_int64, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
+    "dpv_sim3_exp": (C.c_int32, [C.c_int64, vp, vp, vp]),
+    "dpv_sim3_log": (C.c_int32, [C.c_int64, vp, vp, vp]),
     "dpv_block_sparse_solve": (C.c_int32, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
     "dpv_problem_spd_info": (C.c_int32, [vp, c_int64_p]),
     "dpv_proximity_detect": (C.c_int32, [vp, C.c_int64, C.c_int64, C.c_double, vp, C.c_int64,

@@ -146,8 +146,16 @@ struct CorrCfg {
     // kernel at ~1 item/us/SM), 3 consumer groups; C = 256: 3 stages, 1
     // producer, 3 groups
     static constexpr int NS = NS0 >= 6 ? 6 : (NS0 >= 3 ? 3 : (NS0 >= 1 ? NS0 : 1));
+#ifdef DPV_CORR_NP6                 // pipeline-shape experiments (tools/corr_micro.cu)
+    static constexpr int NP = NS == 6 ? DPV_CORR_NP6 : 1;
+#else
     static constexpr int NP = NS == 6 ? 3 : 1;
+#endif
+#ifdef DPV_CORR_NG
+    static constexpr int NG = NS >= DPV_CORR_NG ? DPV_CORR_NG : NS;
+#else
     static constexpr int NG = NS >= 3 ? 3 : NS;
+#endif
     static_assert(NS % NP == 0 && NS % NG == 0, "producers and groups must divide the stages");
     static constexpr int kThreadsT = 32 * NP + NG * kConsumers;
     static constexpr size_t kSmem =
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 32);     // every producer lane arrives (below)
             mbar_init(&empty[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -266,7 +274,9 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
                 M->jj = jjc;
                 M->e = e;
             }
-            __syncwarp();
+            // each lane publishes its own metadata writes with its own
+            // (release) arrival; lane 0's also carries the TMA byte count
+            if (lane != 0) mbar_arrive(&full[s]);
             if (lane == 0) {
                 unsigned char* st = sm + s * SB;
                 const unsigned tx = NH * kGHalfBytes + (staged ? NH * kWin * kWin * 128 : 0);

@@ -13,7 +13,9 @@ enough (verified with a call-counting probe):
   ``patchslam.graph`` (graph.py:29-38) and ``patchslam.synthetic``
   (synthetic.py:17-25) besides ``patchslam.geometry``;
 * ``block_cholesky`` is bound by name in ``patchslam.ba`` (ba.py:22);
-* ``ba._BACKENDS`` (ba.py:490) holds the original solver objects.
+* ``ba._BACKENDS`` (ba.py:490) holds the original solver objects;
+* the pose-graph functions (``patchslam.posegraph``) are replaced by the
+  device versions of ``posegraph.py`` here.
 
 ``loop``, ``pipeline`` and ``cli`` use ``from . import ba`` plus attribute
 access, so they follow the patched module.  Exceptions need no mapping: when
@@ -29,12 +31,16 @@ import importlib
 
 BA_NAMES = ("BAProblem", "residuals", "objective", "assemble", "solve", "solve_dense",
             "solve_block_sparse", "_apply_step", "select_backend")
+# Sim(3) pose-graph optimisation (posegraph.py:85-196); PoseGraphProblem and
+# the reference value types stay: the device functions accept them
+PGO_NAMES = ("objective", "residual_smooth", "residual_loop", "residual_and_jacobian", "optimize")
 
 
 def install():
     """Patch the reference modules in place; returns a zero-argument restore()."""
-    from . import ba, block_cholesky, geometry
+    from . import ba, block_cholesky, geometry, posegraph
     rba = importlib.import_module("patchslam.ba")
+    rpg = importlib.import_module("patchslam.posegraph")
     rgeo = importlib.import_module("patchslam.geometry")
     rgraph = importlib.import_module("patchslam.graph")
     rsyn = importlib.import_module("patchslam.synthetic")
@@ -49,6 +55,8 @@ def install():
         put(mod, "reproject_grid", geometry.reproject_grid)
     for name in BA_NAMES:
         put(rba, name, getattr(ba, name))
+    for name in PGO_NAMES:
+        put(rpg, name, getattr(posegraph, name))
     put(rba, "block_cholesky", block_cholesky.block_cholesky)
     put(rbc, "block_cholesky", block_cholesky.block_cholesky)
     backends = dict(rba._BACKENDS)

@@ -12,7 +12,8 @@ reports how many of this package's kernels ran.
 Modules (VERDICT r1 "Next round" 3): test_ba.py (LM, Schur vs
 full normal equations, dense vs block-sparse, SingularSystem escalation),
 test_block_cholesky.py, test_geometry.py (reprojection and Jacobians vs finite
-differences), test_loop.py (global BA after closure).
+differences), test_loop.py (global BA after closure), test_posegraph.py
+(Sim(3) pose-graph LM, residuals, Jacobians vs finite differences).
 """
 
 import json
@@ -35,7 +36,8 @@ if not os.path.isdir(os.path.join(REF, "patchslam")) or not os.path.isdir(REF_TE
     pytest.skip("reference package not staged in baseline/_ref (run build())",
                 allow_module_level=True)
 
-MODULES = ["test_ba.py", "test_block_cholesky.py", "test_geometry.py", "test_loop.py"]
+MODULES = ["test_ba.py", "test_block_cholesky.py", "test_geometry.py", "test_loop.py",
+           "test_posegraph.py"]
 
 
 @pytest.mark.parametrize("module", MODULES)
