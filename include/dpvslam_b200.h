@@ -266,6 +266,26 @@ int32_t dpv_cholesky_solve(double* a, double* b, int64_t n, int32_t* status_dev,
 int32_t dpv_block_fill_count(const int64_t* keys, int64_t n_keys, int64_t n, int64_t* count);
 
 /* ------------------------------------------------------------------------
+ * Synthetic inputs on the device.
+ * dpv_fill_flow: the flow oracle fill_flow (synthetic.py:222-287) for the
+ * n edges sel (DEVICE int64, NULL = edges 0..n-1): ground-truth reprojection
+ * of each source patch grid (rot (F,9) row-major / trans (F,3) ground-truth
+ * poses, landmarks (L,3), patch_landmark (n_patches) int64), plus the host
+ * generator's draws shift (n,2), outlier (n) uint8, gross (n,2); writes
+ * target (n, cells, 2) and conf (n, 2).  Bit-identical to the reference's
+ * numpy expressions.  All arrays DEVICE.
+ * dpv_reproject_exact: initial targets = reprojection at the current state
+ * (graph.py:152-164) with patch inverse depths patch_depth (n_patches). */
+int32_t dpv_fill_flow(const dpv_graph* g, const double* rot, const double* trans,
+                      const double* landmarks, const int64_t* patch_landmark, const int64_t* sel,
+                      int64_t n, const double* shift, const uint8_t* outlier, const double* gross,
+                      double low_confidence, double width, double height, double* target,
+                      double* conf, void* stream);
+int32_t dpv_reproject_exact(const dpv_graph* g, const double* rot, const double* trans,
+                            const double* patch_depth, const int64_t* sel, int64_t n, double* pix,
+                            void* stream);
+
+/* ------------------------------------------------------------------------
  * Sim(3) pose-graph optimisation (posegraph.py:121-196, optimize; SURVEY
  * 8(f) rank 4).  Similarities as 8 doubles [tx ty tz qx qy qz qw s]
  * (x -> s R x + t; the g2o field order, posegraph.py:12-14).  Constraint c:

@@ -103,21 +103,7 @@ class BAProblem:
 
     def _graph_view(self):
         """The graph's device mirror as the C-ABI's dpv_graph view."""
-        mir = self._g.device()
-        g = _lib.DpvGraph()
-        g.n_frames = self._g.n_frames
-        g.cells = self._g.patch_size ** 2
-        g.n_patches = self._g.n_patches
-        g.n_edges = self._g.n_edges
-        g.patch_grid = mir["patch_grid"].data_ptr()
-        g.edge_src = mir["edge_src"].data_ptr() if g.n_edges else 0
-        g.edge_gpatch = mir["edge_gpatch"].data_ptr() if g.n_edges else 0
-        g.edge_dst = mir["edge_dst"].data_ptr() if g.n_edges else 0
-        g.edge_target = mir["edge_target"].data_ptr() if g.n_edges else 0
-        g.edge_conf = mir["edge_conf"].data_ptr() if g.n_edges else 0
-        for i, v in enumerate(self._g.intrinsics.as_array()):
-            g.intr[i] = float(v)
-        return g
+        return self._g.dpv_view()
 
     def _ensure(self):
         if self._handle is not None:

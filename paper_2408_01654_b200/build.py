@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdpvslam_b200.so")
-SOURCES = ["capi.cu", "problem.cu", "assemble.cu", "solve.cu", "cholesky.cu", "geometry.cu", "corr.cu", "corr_tma.cu", "spd.cu", "loop.cu", "pgo.cu"]
+SOURCES = ["capi.cu", "problem.cu", "assemble.cu", "solve.cu", "cholesky.cu", "geometry.cu", "corr.cu", "corr_tma.cu", "spd.cu", "loop.cu", "pgo.cu", "synth.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]

@@ -527,6 +527,25 @@ class PatchGraph:
             self._edge_clean = ne
         return mir
 
+    def dpv_view(self):
+        """The device mirror as the C-ABI's dpv_graph view (syncs it first)."""
+        from . import _lib
+        mir = self.device()
+        g = _lib.DpvGraph()
+        g.n_frames = self.n_frames
+        g.cells = self.patch_size ** 2
+        g.n_patches = self.n_patches
+        g.n_edges = self.n_edges
+        g.patch_grid = mir["patch_grid"].data_ptr()
+        g.edge_src = mir["edge_src"].data_ptr() if g.n_edges else 0
+        g.edge_gpatch = mir["edge_gpatch"].data_ptr() if g.n_edges else 0
+        g.edge_dst = mir["edge_dst"].data_ptr() if g.n_edges else 0
+        g.edge_target = mir["edge_target"].data_ptr() if g.n_edges else 0
+        g.edge_conf = mir["edge_conf"].data_ptr() if g.n_edges else 0
+        for i, v in enumerate(self.intrinsics.as_array()):
+            g.intr[i] = float(v)
+        return g
+
     def _mirror_poses_written(self, q_dev, t_dev, rows, depth_rows_dev=None):
         """Keep the device mirror current after a device-side write-back."""
         if self._mirror is not None and self._mirror.get("pose_ver") == self._pose_ver - 1:

@@ -19,6 +19,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import ctypes as C
+
 import numpy as np
 
 from .errors import InfeasibleVisibility
@@ -260,15 +262,75 @@ def add_loop_edges(graph, n_poses: int, patches: int, seed: int = 0):
 # flow oracle (synthetic.py:222-300)
 
 
+def _device_available() -> bool:
+    try:
+        import torch
+        return bool(torch.cuda.is_available())
+    except Exception:       # torch missing: host generator
+        return False
+
+
+def _draws(rng, config: OracleConfig, n: int):
+    """The flow oracle's random draws, in the reference's order
+    (synthetic.py:263-268)."""
+    shift = (rng.normal(0.0, config.pixel_noise_sigma, size=(n, 2))
+             if config.pixel_noise_sigma > 0 else np.zeros((n, 2)))
+    outlier = rng.random(n) < config.outlier_fraction
+    ang = rng.uniform(0, 2 * np.pi, size=n)
+    gross = config.outlier_magnitude * np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    return shift, outlier, gross
+
+
+def _fill_flow_device(graph, scene, config, idx, rng):
+    """fill_flow with the reprojection / observability / target assembly on
+    the device (dpv_fill_flow, csrc/synth.cu; bit-identical to the host
+    expressions) and the draws from the host generator."""
+    import torch
+
+    from . import _lib
+    n = len(idx)
+    shift, outlier, gross = _draws(rng, config, n)
+    rot = quat_to_matrix(np.stack([p.q for p in scene.gt_poses])).reshape(-1, 9)
+    gt_t = np.stack([p.t for p in scene.gt_poses])
+    g = graph.dpv_view()
+    mir = graph.device()
+    dev = "cuda"
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)   # noqa: E731
+    rot_d, t_d, lms_d = T(rot), T(gt_t), T(scene.landmarks)
+    plm_d = T(graph._lm.view.astype(np.int64))
+    sel_d = T(idx.astype(np.int64))
+    shift_d, out_d, gross_d = T(shift), T(outlier.astype(np.uint8)), T(gross)
+    m = graph.patch_size ** 2
+    target = torch.empty((n, m, 2), dtype=torch.float64, device=dev)
+    conf = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    w, h = scene.spec.image_size
+    _lib.check(_lib.lib().dpv_fill_flow(
+        C.byref(g), _lib.ptr(rot_d), _lib.ptr(t_d), _lib.ptr(lms_d), _lib.ptr(plm_d),
+        _lib.ptr(sel_d), n, _lib.ptr(shift_d), _lib.ptr(out_d), _lib.ptr(gross_d),
+        float(config.low_confidence), float(w), float(h), _lib.ptr(target), _lib.ptr(conf),
+        _lib.stream_ptr()), "fill_flow")
+    # the mirror stays current (scatter on the device), the host truth by D2H
+    mir["edge_target"][sel_d] = target
+    mir["edge_conf"][sel_d] = conf
+    graph._tgt.view[idx] = target.cpu().numpy()
+    graph._conf.view[idx] = conf.cpu().numpy()
+
+
 def fill_flow(graph, scene, config: OracleConfig = OracleConfig(), edge_indices=None,
-              seed: int = 0) -> None:
+              seed: int = 0, device: bool | None = None) -> None:
     """Ground-truth reprojection + one Gaussian shift per edge, seeded
-    outliers with low confidence, unobservable edges at confidence 0."""
+    outliers with low confidence, unobservable edges at confidence 0.
+    ``device`` (default: when CUDA is available) runs the geometry on the
+    B200 (dpv_fill_flow); the result is bit-identical either way."""
     idx = (np.arange(graph.n_edges) if edge_indices is None
            else np.asarray(list(edge_indices), dtype=np.int64))
     if len(idx) == 0:
         return
     rng = np.random.default_rng(seed)
+    if device is None:
+        device = _device_available()
+    if device:
+        return _fill_flow_device(graph, scene, config, idx, rng)
     intr = graph.intrinsics
     gt_q = np.stack([p.q for p in scene.gt_poses])
     gt_t = np.stack([p.t for p in scene.gt_poses])
@@ -294,11 +356,7 @@ def fill_flow(graph, scene, config: OracleConfig = OracleConfig(), edge_indices=
             & (pix[..., 0] > -slack).all(axis=1) & (pix[..., 0] < w + slack).all(axis=1)
             & (pix[..., 1] > -slack).all(axis=1) & (pix[..., 1] < h + slack).all(axis=1))
         pix_all[lo:lo + len(sel)] = pix
-    shift = (rng.normal(0.0, config.pixel_noise_sigma, size=(n, 2))
-             if config.pixel_noise_sigma > 0 else np.zeros((n, 2)))
-    outlier = rng.random(n) < config.outlier_fraction
-    ang = rng.uniform(0, 2 * np.pi, size=n)
-    gross = config.outlier_magnitude * np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    shift, outlier, gross = _draws(rng, config, n)
     target = pix_all + shift[:, None, :]
     bad = outlier & obs
     target[bad] = target[bad] + gross[bad][:, None, :]
