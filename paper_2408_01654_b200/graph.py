@@ -18,7 +18,7 @@ from __future__ import annotations
 import numpy as np
 
 from .errors import InconsistentFrameId, IndexOutOfRange
-from .geometry import DEFAULT_PATCH_SIZE, Intrinsics, Patch, Pose, pinhole_rays, quat_to_matrix
+from .geometry import DEFAULT_PATCH_SIZE, Intrinsics, Patch, Pose, pinhole_rays
 
 ODOMETRY = "odometry"   # graph.py:40
 LOOP = "loop"           # graph.py:41
@@ -350,7 +350,8 @@ class PatchGraph:
 
     def add_edges(self, triples, kind: str = ODOMETRY) -> list[int]:
         """Append edges (i, k, j); targets start at the current reprojection
-        (computed on the GPU) with confidence (1, 1) (graph.py:144-165)."""
+        with confidence (1, 1) (graph.py:144-165), computed on the GPU
+        (dpv_reproject_exact, bit-identical to the reference's expression)."""
         tri = np.asarray(list(triples), dtype=np.int64).reshape(-1, 3)
         if len(tri) == 0:
             return []
@@ -360,14 +361,13 @@ class PatchGraph:
             self._check_edge_indices(i, k, j)
         if kind == LOOP and np.any(tri[:, 0] == tri[:, 2]):
             raise ValueError("loop edges must connect distinct frames")
-        from .geometry import reproject_grid
+        from .synthetic import reproject_targets
         src, pat, dst = tri[:, 0], tri[:, 1], tri[:, 2]
-        gids = np.asarray(self._poff, dtype=np.int64)[src] + pat
-        rays = pinhole_rays(self._grid.view[gids], self.intrinsics)
-        rot = quat_to_matrix(self._q.view)
-        pix, _ = reproject_grid(rays, self._depth.view[gids], rot[src], self._t.view[src],
-                                rot[dst], self._t.view[dst], self.intrinsics)
-        return self.add_edge_arrays(src, pat, dst, pix, np.ones((len(tri), 2)), kind)
+        m = self.patch_size ** 2
+        ids = self.add_edge_arrays(src, pat, dst, np.zeros((len(tri), m, 2)),
+                                   np.ones((len(tri), 2)), kind)
+        reproject_targets(self, np.asarray(ids, dtype=np.int64))
+        return ids
 
     def add_edge_arrays(self, src, patch, dst, target, conf, kind=ODOMETRY) -> list[int]:
         """Bulk edge append without reprojection (targets supplied)."""

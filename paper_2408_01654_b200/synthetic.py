@@ -223,9 +223,37 @@ def generate(spec: SceneSpec, patches_per_frame: int = 96, odometry_radius: int 
                 graph.add_edge_arrays(tri[:, 0], tri[:, 1], tri[:, 2], np.zeros((len(tri), m, 2)),
                                       np.ones((len(tri), 2)), ODOMETRY)
     if initial_targets and graph.n_edges:
-        _reproject_targets(graph, np.arange(graph.n_edges), graph._q.view, graph._t.view,
-                           graph._depth.view)
+        reproject_targets(graph, np.arange(graph.n_edges))
     return scene, graph
+
+
+def reproject_targets(graph, idx, device=None):
+    """Initial targets of edges idx = the current reprojection of their source
+    patch grids (graph.py:152-164), bit-identical to the reference's numpy
+    expression: on the device (dpv_reproject_exact) when CUDA is available,
+    else the host restatement."""
+    idx = np.asarray(idx, dtype=np.int64)
+    if len(idx) == 0:
+        return
+    if device is None:
+        device = _device_available()
+    if not device:
+        return _reproject_targets(graph, idx, graph._q.view, graph._t.view, graph._depth.view)
+    import torch
+
+    from . import _lib
+    g = graph.dpv_view()
+    mir = graph.device()
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")   # noqa: E731
+    rot_d = T(quat_to_matrix(graph._q.view).reshape(-1, 9))
+    sel_d = T(idx)
+    pix = torch.empty((len(idx), graph.patch_size ** 2, 2), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().dpv_reproject_exact(C.byref(g), _lib.ptr(rot_d), _lib.ptr(mir["t"]),
+                                              _lib.ptr(mir["patch_depth"]), _lib.ptr(sel_d),
+                                              len(idx), _lib.ptr(pix), _lib.stream_ptr()),
+               "reproject_exact")
+    mir["edge_target"][sel_d] = pix
+    graph._tgt.view[idx] = pix.cpu().numpy()
 
 
 def _reproject_targets(graph, idx, q, t, patch_depth):

@@ -76,3 +76,18 @@ def test_reproject_exact_matches_host_targets():
                                               _lib.ptr(d_d), None, graph.n_edges, _lib.ptr(pix),
                                               _lib.stream_ptr()), "reproject_exact")
     assert np.array_equal(pix.cpu().numpy(), want)
+
+
+def test_add_edges_targets_bit_exact():
+    """PatchGraph.add_edges / connect_frame targets (graph.py:144-176) on the
+    device equal the reference expression restated on the host."""
+    spec = synthetic.SceneSpec(kind="circle", n_frames=18, seed=5, n_landmarks=3000,
+                               look="inward")
+    _, graph = synthetic.generate(spec, patches_per_frame=16, odometry_radius=0,
+                                  initial_targets=False)
+    synthetic.perturb_poses(graph, 0.02, seed=3)
+    ids = graph.connect_frame(17, 6) + graph.add_edges([(2, 3, 15), (15, 0, 2)], "loop")
+    got = graph._tgt.view[ids].copy()
+    assert np.array_equal(graph.device()["edge_target"].cpu().numpy()[ids], got)
+    synthetic.reproject_targets(graph, np.asarray(ids), device=False)
+    assert np.array_equal(graph._tgt.view[ids], got)
