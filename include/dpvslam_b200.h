@@ -284,6 +284,14 @@ int32_t dpv_fill_flow(const dpv_graph* g, const double* rot, const double* trans
 int32_t dpv_reproject_exact(const dpv_graph* g, const double* rot, const double* trans,
                             const double* patch_depth, const int64_t* sel, int64_t n, double* pix,
                             void* stream);
+/* visible_landmarks (synthetic.py:68-79) of every frame: inverse ground-truth
+ * poses inv_q (F,4) / inv_t (F,3), landmarks (L,3), intr HOST [fx fy cx cy];
+ * flags (F, L) uint8 = in front (z > 0.5) and inside the image by `margin`
+ * (u in [margin, u_max], v in [margin, v_max]).  Bit-identical tests. */
+int32_t dpv_visible_landmarks(int64_t n_frames, int64_t n_landmarks, const double* inv_q,
+                              const double* inv_t, const double* landmarks, const double* intr,
+                              double margin, double u_max, double v_max, uint8_t* flags,
+                              void* stream);
 
 /* ------------------------------------------------------------------------
  * Sim(3) pose-graph optimisation (posegraph.py:121-196, optimize; SURVEY

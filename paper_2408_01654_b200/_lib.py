@@ -101,6 +101,8 @@ SIGNATURES = {
     "dpv_fill_flow": (C.c_int32, [C.c_void_p, vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp,
                                   C.c_double, C.c_double, C.c_double, vp, vp, vp]),
     "dpv_reproject_exact": (C.c_int32, [C.c_void_p, vp, vp, vp, vp, C.c_int64, vp, vp]),
+    "dpv_visible_landmarks": (C.c_int32, [C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_double,
+                                          C.c_double, C.c_double, vp, vp]),
     "dpv_sim3_exp": (C.c_int32, [C.c_int64, vp, vp, vp]),
     "dpv_sim3_log": (C.c_int32, [C.c_int64, vp, vp, vp]),
     "dpv_block_sparse_solve": (C.c_int32, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),

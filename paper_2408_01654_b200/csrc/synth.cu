@@ -126,6 +126,39 @@ __global__ void k_reproject_exact(int64_t n, const int64_t* __restrict__ sel,
     }
 }
 
+// visible_landmarks for every frame at once (synthetic.py:68-79): camera
+// points inv_pose.act(L) = L + w t + u x t (t = 2 u x L) + inv_t with
+// numpy's np.cross (a1 b2 - a2 b1, no contraction), projection, the depth /
+// margin tests.  One thread per (frame, landmark); flags (F, L) uint8.
+__global__ void k_visible(int64_t F, int64_t L, const double* __restrict__ inv_q,
+                          const double* __restrict__ inv_t, const double* __restrict__ lms,
+                          double fx, double fy, double cx, double cy, double margin, double umax,
+                          double vmax, uint8_t* __restrict__ flags) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < F * L;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = x / L, l = x % L;
+        const double* q = inv_q + 4 * f;
+        const double v0 = lms[3 * l], v1 = lms[3 * l + 1], v2 = lms[3 * l + 2];
+        const double u0 = q[0], u1 = q[1], u2 = q[2], w = q[3];
+        const double t0 = mul(2.0, sub(mul(u1, v2), mul(u2, v1)));
+        const double t1 = mul(2.0, sub(mul(u2, v0), mul(u0, v2)));
+        const double t2 = mul(2.0, sub(mul(u0, v1), mul(u1, v0)));
+        const double c0 = sub(mul(u1, t2), mul(u2, t1));
+        const double c1 = sub(mul(u2, t0), mul(u0, t2));
+        const double c2 = sub(mul(u0, t1), mul(u1, t0));
+        const double* it = inv_t + 3 * f;
+        const double px = add(add(add(v0, mul(w, t0)), c0), it[0]);
+        const double py = add(add(add(v1, mul(w, t1)), c1), it[1]);
+        const double pz = add(add(add(v2, mul(w, t2)), c2), it[2]);
+        const bool valid = pz > 1e-8;
+        const double zs = valid ? pz : 1.0;
+        const double u = add(dvd(mul(fx, px), zs), cx);
+        const double v = add(dvd(mul(fy, py), zs), cy);
+        flags[x] = (valid && pz > 0.5 && u >= margin && u <= umax && v >= margin && v <= vmax)
+                       ? 1 : 0;
+    }
+}
+
 }  // namespace
 }  // namespace dpv
 
@@ -173,6 +206,25 @@ int32_t dpv_reproject_exact(const dpv_graph* g, const double* rot, const double*
                                                         g->edge_gpatch, g->patch_grid, rot, trans,
                                                         patch_depth, g->intr[0], g->intr[1],
                                                         g->intr[2], g->intr[3], g->cells, pix);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+    DPV_ABI_CATCH
+}
+
+int32_t dpv_visible_landmarks(int64_t n_frames, int64_t n_landmarks, const double* inv_q,
+                              const double* inv_t, const double* landmarks, const double* intr,
+                              double margin, double u_max, double v_max, uint8_t* flags,
+                              void* stream) {
+    DPV_ABI_TRY
+    clear_error();
+    DPV_ARG(n_frames >= 0 && n_landmarks >= 0 && intr, "bad visible_landmarks args");
+    if (n_frames == 0 || n_landmarks == 0) return DPV_OK;
+    DPV_ARG(inv_q && inv_t && landmarks && flags, "NULL visible_landmarks argument");
+    cudaStream_t st = as_stream(stream);
+    DPV_TSTART("visible_landmarks", st);
+    k_visible<<<grid_for(n_frames * n_landmarks, 256), 256, 0, st>>>(
+        n_frames, n_landmarks, inv_q, inv_t, landmarks, intr[0], intr[1], intr[2], intr[3], margin,
+        u_max, v_max, flags);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
     DPV_ABI_CATCH

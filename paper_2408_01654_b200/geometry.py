@@ -206,6 +206,16 @@ class Intrinsics:
         return np.array([self.fx, self.fy, self.cx, self.cy])
 
 
+def square_grids(centers, patch_size: int = DEFAULT_PATCH_SIZE):
+    """square_grid of many keypoints at once (n, p*p, 2); the same additions,
+    so bit-identical to stacking square_grid per keypoint."""
+    centers = np.asarray(centers, dtype=float).reshape(-1, 2)
+    offs = np.arange(patch_size) - (patch_size - 1) / 2.0
+    gy, gx = np.meshgrid(offs, offs, indexing="ij")
+    return np.stack([gx.ravel()[None, :] + centers[:, 0:1], gy.ravel()[None, :] + centers[:, 1:2]],
+                    axis=-1)
+
+
 def square_grid(center, patch_size: int = DEFAULT_PATCH_SIZE):
     """Row-major p x p unit grid around a keypoint (geometry.py:398-407)."""
     center = np.asarray(center, dtype=float).reshape(2)

@@ -24,7 +24,7 @@ import ctypes as C
 import numpy as np
 
 from .errors import InfeasibleVisibility
-from .geometry import Intrinsics, Pose, matrix_to_quat, pinhole_rays, quat_to_matrix, square_grid
+from .geometry import Intrinsics, Pose, matrix_to_quat, pinhole_rays, quat_to_matrix, square_grids
 from .graph import LOOP, ODOMETRY, PatchGraph
 
 DEFAULT_INTRINSICS = Intrinsics(320.0, 320.0, 256.0, 192.0)   # synthetic.py:28
@@ -203,8 +203,9 @@ def generate(spec: SceneSpec, patches_per_frame: int = 96, odometry_radius: int 
     margin = (patch_size - 1) / 2.0 + 0.5
     m = patch_size * patch_size
     counts = np.zeros(spec.n_frames, dtype=np.int64)
+    vis_all = _visible_all(scene, margin) if _device_available() else None
     for fid in range(spec.n_frames):
-        vis = scene.visible_landmarks(fid, margin)
+        vis = vis_all[fid] if vis_all is not None else scene.visible_landmarks(fid, margin)
         if len(vis) < patches_per_frame:
             raise InfeasibleVisibility(
                 f"frame {fid} sees {len(vis)} landmarks < {patches_per_frame};"
@@ -212,8 +213,8 @@ def generate(spec: SceneSpec, patches_per_frame: int = 96, odometry_radius: int 
         chosen = rng.choice(vis, size=patches_per_frame, replace=False)
         cam = scene.camera_points(fid, chosen)
         pix, _ = _project(cam, spec.intrinsics)
-        grids = np.stack([square_grid(pix[i], patch_size) for i in range(patches_per_frame)])
-        depths = np.array([float(1.0 / cam[i, 2]) for i in range(patches_per_frame)])
+        grids = square_grids(pix, patch_size)
+        depths = 1.0 / cam[:, 2]
         graph.add_frame_arrays(gt[fid].q, gt[fid].t, fid * spec.frame_dt, grids, depths,
                                chosen.astype(np.int64))
         counts[fid] = patches_per_frame
@@ -288,6 +289,30 @@ def add_loop_edges(graph, n_poses: int, patches: int, seed: int = 0):
 
 # ---------------------------------------------------------------------------
 # flow oracle (synthetic.py:222-300)
+
+
+def _visible_all(scene, margin):
+    """visible_landmarks (synthetic.py:68-79) of every frame in one device
+    pass (dpv_visible_landmarks, bit-identical tests); per frame the sorted
+    landmark ids, as np.nonzero returns them."""
+    import torch
+
+    from . import _lib
+    invs = [p.inverse() for p in scene.gt_poses]
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")  # noqa
+    inv_q, inv_t = T(np.stack([p.q for p in invs])), T(np.stack([p.t for p in invs]))
+    lms = T(scene.landmarks)
+    F, L = len(invs), len(scene.landmarks)
+    w, h = scene.spec.image_size
+    intr = np.ascontiguousarray(scene.intrinsics.as_array(), dtype=np.float64)
+    flags = torch.empty((F, L), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().dpv_visible_landmarks(
+        F, L, _lib.ptr(inv_q), _lib.ptr(inv_t), _lib.ptr(lms), intr.ctypes.data_as(C.c_void_p),
+        float(margin), float(w - 1 - margin), float(h - 1 - margin), _lib.ptr(flags),
+        _lib.stream_ptr()), "visible_landmarks")
+    counts = flags.sum(dim=1, dtype=torch.int64).cpu().numpy()
+    ids = torch.nonzero(flags)[:, 1].cpu().numpy()
+    return np.split(ids, np.cumsum(counts)[:-1])
 
 
 def _device_available() -> bool:
