@@ -839,148 +839,6 @@ __global__ void __launch_bounds__(128, MINB) k_key_blocks(
     }
 }
 
-// The same blocks with FOUR consecutive union keys per warp.  Keys are sorted
-// by (a, b), so a group usually shares its row var a; when it does and each
-// key has one pair run (the banded part of a patch graph: the rows shared by
-// a and b are the patches of the frames [b - r, a + r], contiguous in both
-// incidence lists), the warp walks the union of the four runs over var a's
-// incidence list once: each U block is loaded once for the four keys and
-// each key's V block only inside its own run (one L2 gather per pair instead
-// of two; 4 keys x 4 accumulator chains).  Other groups take the per-key loop.
-template <int UNR>
-__device__ __forceinline__ void schur_runs(int64_t w, int lane, const int32_t* key_run_ptr,
-                                           const int32_t* run_l, const int32_t* run_r,
-                                           const int32_t* run_len, const double* uinc,
-                                           const double* inc_block, double (&c)[4][2]) {
-    const int kq = lane & 3, ci = lane >> 2;
-    for (int32_t q = key_run_ptr[w]; q < key_run_ptr[w + 1]; ++q) {
-        const int32_t len = run_len[q];
-        const double* ub = uinc + (int64_t)run_l[q] * 6;
-        const double* vb = inc_block + (int64_t)run_r[q] * 6;
-        for (int32_t t0 = 0; t0 < len; t0 += 4 * UNR) {
-            double a[UNR], b[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int32_t t = t0 + 4 * u + kq;
-                const bool ok = t < len && ci < 6;
-                a[u] = ok ? __ldg(ub + (int64_t)t * 6 + ci) : 0.0;
-                b[u] = ok ? __ldg(vb + (int64_t)t * 6 + ci) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) dmma_f64(c[u & 3][0], c[u & 3][1], a[u], b[u]);
-        }
-    }
-}
-
-template <int UNR, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_key_blocks4(
-    int64_t W, const int32_t* key_seg_ptr, const int32_t* key_seg, const double* seg_h,
-    const int32_t* __restrict__ key_run_ptr, const int32_t* __restrict__ run_l,
-    const int32_t* __restrict__ run_r, const int32_t* __restrict__ run_len,
-    const int32_t* __restrict__ key_a, const double* __restrict__ uinc,
-    const double* __restrict__ inc_block, double* __restrict__ pose_blocks,
-    double* __restrict__ schur_blocks) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t G = (W + 3) / 4;
-    const int kq = lane & 3, ci = lane >> 2, oi = lane >> 2;
-    for (int64_t g = warp; g < G; g += nwarps) {
-        const int64_t w0 = 4 * g;
-        const int nk = (int)min((int64_t)4, W - w0);
-        // pose blocks (ba.py:389-394), key by key
-        for (int j = 0; j < nk; ++j) {
-            const int64_t w = w0 + j;
-            double h[21];
-#pragma unroll
-            for (int k = 0; k < 21; ++k) h[k] = 0.0;
-            for (int32_t k = key_seg_ptr[w] + lane; k < key_seg_ptr[w + 1]; k += 32) {
-                const int32_t code = key_seg[k];
-                const double sgn = (code & 1) ? -1.0 : 1.0;
-                const double* src = seg_h + (int64_t)(code >> 1) * 21;
-#pragma unroll
-                for (int q = 0; q < 21; ++q) h[q] += sgn * src[q];
-            }
-#pragma unroll
-            for (int q = 0; q < 21; ++q) h[q] = warp_sum(h[q]);
-            for (int idx = lane; idx < 36; idx += 32) {
-                const int a = idx / 6, b = idx % 6;
-                const int t = a <= b ? utri(a, b) : utri(b, a);
-                double v = 0.0;
-#pragma unroll
-                for (int q = 0; q < 21; ++q) v = (q == t) ? h[q] : v;
-                pose_blocks[w * 36 + idx] = v;
-            }
-        }
-        // Schur blocks (ba.py:405-413)
-        const int32_t a0 = key_a[w0];
-        bool fuse = nk > 1;
-        int32_t l[4], r[4], len[4];
-        int32_t lo = INT32_MAX, hi = INT32_MIN;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            l[j] = 0;
-            r[j] = 0;
-            len[j] = 0;
-            if (j < nk) {
-                const int64_t w = w0 + j;
-                const int32_t q = key_run_ptr[w];
-                fuse = fuse && key_a[w] == a0 && key_run_ptr[w + 1] - q == 1;
-                if (key_run_ptr[w + 1] - q >= 1) {
-                    l[j] = run_l[q];
-                    r[j] = run_r[q];
-                    len[j] = run_len[q];
-                    lo = min(lo, l[j]);
-                    hi = max(hi, l[j] + len[j]);
-                }
-            }
-        }
-        double c[4][4][2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) c[j][k][0] = c[j][k][1] = 0.0;
-        if (fuse) {
-            for (int32_t u0 = lo; u0 < hi; u0 += 4 * UNR) {
-                double a[UNR], b[4][UNR];
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    const int32_t t = u0 + 4 * u + kq;
-                    const bool ok = t < hi && ci < 6;
-                    a[u] = ok ? __ldg(uinc + (int64_t)t * 6 + ci) : 0.0;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const bool in = ok && t >= l[j] && t < l[j] + len[j];
-                        b[j][u] = in ? __ldg(inc_block + (int64_t)(r[j] + (t - l[j])) * 6 + ci)
-                                     : 0.0;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        dmma_f64(c[j][u & 3][0], c[j][u & 3][1], a[u], b[j][u]);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j < nk)
-                    schur_runs<UNR>(w0 + j, lane, key_run_ptr, run_l, run_r, run_len, uinc,
-                                    inc_block, c[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (j >= nk) break;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int oj = 2 * (lane & 3) + h;
-                const double v = (c[j][0][h] + c[j][1][h]) + (c[j][2][h] + c[j][3][h]);
-                if (oi < 6 && oj < 6) schur_blocks[(w0 + j) * 36 + oi * 6 + oj] = v;
-            }
-        }
-    }
-}
-
 // Grouped Schur complement: per chunk of rows sharing one incidence-var list
 // (v_0 < ... < v_{m-1}), stage W (6m x nr: var j's 6 components on rows
 // 6j..6j+5, columns = rows of the chunk) in shared memory and form the upper
@@ -1367,21 +1225,12 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
             p->run_len, p->uinc, p->inc_block, p->pose_blocks, p->schur_blocks, 0);
         DPV_CHECK_LAUNCH();
     } else if (p->W > 0) {
+        int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
         DPV_TSTART("key_blocks", st);
-        if (!p->grouped) {
-            const int64_t groups = (p->W + 3) / 4;
-            const int blocks = (int)std::min<int64_t>((groups + 3) / 4, (int64_t)sm_count() * 64);
-            k_key_blocks4<4, 3><<<blocks, 128, 0, st>>>(
-                p->W, p->key_seg_ptr, p->key_seg, p->seg_h, p->key_run_ptr, p->run_l, p->run_r,
-                p->run_len, p->key_a, p->uinc, p->inc_block, p->pose_blocks, p->schur_blocks);
-        } else {
-            const int blocks = (int)std::min<int64_t>((p->W + 3) / 4, (int64_t)sm_count() * 64);
-            k_key_blocks<16, 3><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg,
-                                                        p->seg_h, p->key_run_ptr, p->run_l,
-                                                        p->run_r, p->run_len, p->uinc,
-                                                        p->inc_block, p->pose_blocks,
-                                                        p->schur_blocks, 1);
-        }
+        k_key_blocks<16, 3><<<blocks, 128, 0, st>>>(p->W, p->key_seg_ptr, p->key_seg, p->seg_h,
+                                                    p->key_run_ptr, p->run_l, p->run_r,
+                                                    p->run_len, p->uinc, p->inc_block,
+                                                    p->pose_blocks, p->schur_blocks, p->grouped);
         DPV_CHECK_LAUNCH();
         if (p->grouped) {
             static size_t cur = 0;
