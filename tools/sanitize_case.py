@@ -1,7 +1,9 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
 synccheck): a 60-pose loop-closure global BA (block-sparse backend ->
 spd.cu's flag dataflow, both levels), a cfg1-shaped window BA (small dense
-solver) and a two-level bf16 correlation (corr_tma.cu mbarriers / TMA).
+solver), a two-level bf16 correlation (corr_tma.cu mbarriers / TMA), a Sim(3)
+pose-graph LM (pgo.cu + the dense K4c engine) and device input generation
+(synth.cu).
 
     compute-sanitizer --tool racecheck python tools/sanitize_case.py
 """
@@ -41,6 +43,23 @@ def main():
     out = corr.corr(gm, corr.pyramid(f), coords, ii, jj)
     torch.cuda.synchronize()
     print("corr:", tuple(out.shape), float(out.abs().sum()))
+    # Sim(3) pose-graph LM (pgo.cu) on a golden problem, device input
+    # generation (synth.cu: visibility, flow oracle, initial targets)
+    from paper_2408_01654_b200 import posegraph as PG
+    from paper_2408_01654_b200 import synthetic
+    zp = dict(np.load(os.path.join(ROOT, "tests", "golden", "pgo.npz")))
+    sims = lambda a: [PG.Similarity(r[3:7], r[0:3], float(r[7])) for r in a]   # noqa: E731
+    loops = [(int(j), int(k), d) for (j, k), d in zip(zp["loop_loops"], sims(zp["loop_loopsim"]))]
+    prob = PG.PoseGraphProblem(sims(zp["loop_nodes"]), sims(zp["loop_odo"]), loops)
+    rep = PG.optimize(prob, 10)
+    print("pgo:", rep.iterations, rep.final_objective)
+    spec = synthetic.SceneSpec(kind="circle", n_frames=12, seed=1, n_landmarks=2000,
+                               look="inward")
+    scene, graph = synthetic.generate(spec, patches_per_frame=16, odometry_radius=3,
+                                      initial_targets=True)
+    synthetic.fill_flow(graph, scene, synthetic.OracleConfig(pixel_noise_sigma=0.3,
+                                                             outlier_fraction=0.1), seed=1)
+    print("synth:", graph.n_edges, float(np.abs(graph._tgt.view).sum()))
     print("kernels launched:", _lib.lib().dpv_launch_count() - l0)
 
 
