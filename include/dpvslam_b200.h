@@ -179,6 +179,14 @@ int32_t dpv_reduced_system(dpv_problem* prob, double lam, double* blocks, double
  * dp (n,6), dd (P).  *status_dev (device int32) = 0 ok / 1 not positive definite. */
 int32_t dpv_solve(dpv_problem* prob, double lam, double* dp, double* dd, int32_t* status_dev,
                   void* stream);
+/* The same solve with an explicit backend (ba.py:490 _BACKENDS): 0 = auto
+ * (the fastest: single-CTA dense solve for 6n <= 162, else the banded +
+ * border sparse factorisation), 1 = dense (solve_dense, ba.py:451-472: S in
+ * a dense matrix, every-tile Cholesky on the FP64 tensor cores), 2 = block
+ * sparse (solve_block_sparse, ba.py:475-487: the spd.cu factorisation at
+ * every size). */
+int32_t dpv_solve_backend(dpv_problem* p, double lam, int32_t backend, double* dp, double* dd,
+                          int32_t* status_dev, void* stream);
 /* K2 pixels of every problem edge times `scale` (problem order, (E,m,2)):
  * the reprojected coordinates P' that feed the correlation lookup (pass 0.25
  * for 1/4-resolution feature maps).  Same arithmetic as reproject_grid. */

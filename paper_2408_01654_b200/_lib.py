@@ -88,6 +88,7 @@ SIGNATURES = {
     "dpv_assemble_rest": (C.c_int32, [vp, vp, vp]),
     "dpv_reduced_system": (C.c_int32, [vp, C.c_double, vp, vp, vp, vp]),
     "dpv_solve": (C.c_int32, [vp, C.c_double, vp, vp, vp, vp]),
+    "dpv_solve_backend": (C.c_int32, [vp, C.c_double, C.c_int32, vp, vp, vp, vp]),
     "dpv_back_substitute": (C.c_int32, [vp, C.c_double, vp, vp, vp]),
     "dpv_apply_step": (C.c_int32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "dpv_lm_solve": (C.c_int32, [vp, vp, vp, vp, C.POINTER(DpvLmParams),

@@ -480,7 +480,7 @@ def select_backend(problem: BAProblem, threshold: int = DEFAULT_BACKEND_THRESHOL
     return DENSE if problem.n_free_poses <= threshold else BLOCK_SPARSE
 
 
-def _device_solve(system: BlockSparseSystem, lam):
+def _device_solve(system: BlockSparseSystem, lam, backend: int = 0):
     torch = _torch()
     system._sync()
     p = system._problem
@@ -489,8 +489,9 @@ def _device_solve(system: BlockSparseSystem, lam):
     status = torch.zeros(8, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _lib.check(_lib.lib().dpv_solve(p._ensure(), float(lam), _lib.ptr(dp), _lib.ptr(dd),
-                                    _lib.ptr(status), _lib.stream_ptr()), "solve")
+    _lib.check(_lib.lib().dpv_solve_backend(p._ensure(), float(lam), int(backend), _lib.ptr(dp),
+                                            _lib.ptr(dd), _lib.ptr(status), _lib.stream_ptr()),
+               "solve")
     st = status.cpu().numpy()
     t1 = time.perf_counter()
     if st[0] != 0:
@@ -500,9 +501,10 @@ def _device_solve(system: BlockSparseSystem, lam):
 
 
 def solve_dense(system: BlockSparseSystem, lam: float | None = None):
-    """Schur-reduce and factorise S(lam) (ba.py:451-472) on the B200."""
+    """Schur-reduce and factorise S(lam) (ba.py:451-472) on the B200: S in a
+    dense matrix, every-tile Cholesky (single-CTA for 6n <= 162)."""
     lam = system.damping if lam is None else lam
-    dp, dd, dt = _device_solve(system, lam)
+    dp, dd, dt = _device_solve(system, lam, 1)
     stats = {"backend": DENSE, "factorize_s": dt, "solve_s": 0.0,
              "peak_block_count": system.n_pose * system.n_pose}
     return dp.cpu().numpy(), dd.cpu().numpy(), stats
@@ -515,7 +517,7 @@ def solve_block_sparse(system: BlockSparseSystem, lam: float | None = None):
     test_ba.py:192-201); ``peak_block_count`` is the exact symbolic fill of
     the natural-order block factor."""
     lam = system.damping if lam is None else lam
-    dp, dd, dt = _device_solve(system, lam)
+    dp, dd, dt = _device_solve(system, lam, 2)
     stats = {"backend": BLOCK_SPARSE, "factorize_s": dt, "solve_s": 0.0,
              "peak_block_count": system._problem.block_fill_count()}
     return dp.cpu().numpy(), dd.cpu().numpy(), stats

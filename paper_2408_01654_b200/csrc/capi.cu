@@ -579,6 +579,19 @@ int32_t dpv_solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* s
     DPV_ABI_CATCH
 }
 
+int32_t dpv_solve_backend(dpv_problem* p, double lam, int32_t backend, double* dp, double* dd,
+                          int32_t* status_dev, void* stream) {
+    DPV_ABI_TRY
+    clear_error();
+    DPV_ARG(p && dp && (dd || p->P == 0) && status_dev, "NULL argument");
+    DPV_ARG(backend >= 0 && backend <= 2, "backend must be 0 (auto), 1 (dense) or 2 (sparse)");
+    p->solve_backend = backend;
+    const int32_t s = solve(p, lam, dp, dd, status_dev, as_stream(stream));
+    p->solve_backend = 0;
+    return s;
+    DPV_ABI_CATCH
+}
+
 int32_t dpv_reproject_coords(dpv_problem* p, const double* q, const double* t, const double* d,
                              double scale, double* coords_out, void* stream) {
     DPV_ABI_TRY

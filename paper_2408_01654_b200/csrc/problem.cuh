@@ -167,6 +167,12 @@ struct dpv_problem {
     int32_t* perm_pos = nullptr;   // (n) pose var -> permuted position in the dense solve
     dpv::SpdPlan* spd = nullptr;   // sparse band+border solver plan (lazily built)
     int32_t spd_failed = 0;        // plan impossible -> tile-plan factorisation
+    // explicit backend of the next solve (dpv_solve_backend): 0 = auto (small
+    // dense solve for 6n <= kSmallMax, else the sparse factorisation),
+    // 1 = dense (ba.solve_dense: full dense Cholesky of S), 2 = block sparse
+    int32_t solve_backend = 0;
+    dpv::FactorPlan* dplan = nullptr;   // every-tile plan of the dense backend
+    int32_t* ident_pos = nullptr;       // (n) identity pose order for it
     // the plan is host work (~1 ms at cfg3): built on a host thread started
     // by the index build, joined by the first sparse solve
     std::thread plan_thread;
@@ -209,6 +215,7 @@ struct dpv_problem {
         for (void* p : allocs) cudaFreeAsync(p, alloc_stream);
         if (lm_host) dpv::pinned_slot_put(lm_host);
         delete plan;
+        delete dplan;
         dpv::spd_plan_free(spd);
     }
 };

@@ -575,6 +575,38 @@ int32_t ensure_plan(dpv_problem* p, int64_t N, cudaStream_t st) {
     return DPV_OK;
 }
 
+__global__ void k_iota_pos(int64_t n, int32_t* pos) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        pos[i] = (int32_t)i;
+}
+
+int32_t ensure_dense_buffers(dpv_problem* p, int64_t N) {
+    if (p->dense) return DPV_OK;
+    p->dense_ld = dense_ld(N);
+    DPV_TRY(p->alloc(&p->dense, (N + 1) * p->dense_ld));
+    DPV_TRY(p->alloc(&p->bsub_part, dense_workspace_doubles(N)));
+    return DPV_OK;
+}
+
+// the dense backend's plan: every lower tile, natural pose order
+int32_t ensure_dense_full(dpv_problem* p, int64_t N, cudaStream_t st) {
+    if (!p->dplan) {
+        auto* plan = new (std::nothrow) FactorPlan();
+        DPV_ARG(plan != nullptr, "allocation failed");
+        const int32_t s = build_factor_plan(N, nullptr, *plan);
+        if (s != DPV_OK) {
+            delete plan;
+            return s;
+        }
+        p->dplan = plan;
+        DPV_TRY(p->alloc(&p->ident_pos, p->n));
+        k_iota_pos<<<grid_for(p->n, 256), 256, 0, st>>>(p->n, p->ident_pos);
+        DPV_CHECK_LAUNCH();
+    }
+    return ensure_dense_buffers(p, N);
+}
+
 int32_t ensure_dense(dpv_problem* p, int64_t N, cudaStream_t st) {
     DPV_TRY(ensure_plan(p, N, st));
     if (p->dense) return DPV_OK;
@@ -647,11 +679,33 @@ void spd_plan_prefetch(dpv_problem* p) {
     });
 }
 
+// S(lam) scattered into the augmented dense matrix in the order `pos`,
+// factorised and solved by the tile engine following `plan`; dp in pose order
+static int32_t dense_path(dpv_problem* p, double lam, int64_t N, const FactorPlan& plan,
+                          const int32_t* pos, double* dp, int32_t* status, cudaStream_t st) {
+    const int64_t ld = p->dense_ld;
+    DPV_CUDA(cudaMemsetAsync(p->dense, 0, sizeof(double) * (N + 1) * ld, st));
+    DPV_TSTART("dense_scatter", st);
+    k_dense_scatter<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
+        p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld, pos);
+    DPV_CHECK_LAUNCH();
+    DPV_TSTART("dense_pin_rhs", st);
+    k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam, p->scal,
+                                                       p->dense, ld, pos);
+    DPV_CHECK_LAUNCH();
+    DPV_TRY(dense_factor_solve(p->dense, ld, N, status, p->red_rhs, p->bsub_part, plan, st));
+    DPV_TSTART("unpermute", st);
+    k_unpermute<<<grid_for(N, 256), 256, 0, st>>>(p->n, pos, p->red_rhs, dp);
+    DPV_CHECK_LAUNCH();
+    return DPV_OK;
+}
+
 int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* status,
               cudaStream_t st) {
     const int64_t N = 6 * p->n;
     DPV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 2, st));
-    if (N <= kSmallMax) {
+    const int32_t backend = p->solve_backend;
+    if (N <= kSmallMax && backend != 2) {
         const size_t smem = sizeof(double) * (size_t)(N + 1) * (N + 1);
         DPV_TSTART("small_solve", st);
         static size_t cur = 0;
@@ -660,6 +714,11 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
             p->n, p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, p->rhs_pose,
             p->rhs_schur, p->scal, lam, dp, status);
         DPV_CHECK_LAUNCH();
+    } else if (backend == 1) {
+        // ba.solve_dense (ba.py:451-472): S scattered into a dense matrix in
+        // natural pose order, every-tile right-looking Cholesky (cholesky.cu)
+        DPV_TRY(ensure_dense_full(p, N, st));
+        DPV_TRY(dense_path(p, lam, N, *p->dplan, p->ident_pos, dp, status, st));
     } else if (!p->spd_failed) {
         // banded + border sparse factorisation (spd.cu)
         if (!p->spd && p->plan_thread.joinable()) {
@@ -694,22 +753,7 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
         DPV_TRY(spd_factor_solve(p->spd, p->key_a, p->key_b, p->sblk, p->red_rhs, dp, status, st));
     } else {
         DPV_TRY(ensure_dense(p, N, st));
-        const int64_t ld = p->dense_ld;
-        DPV_CUDA(cudaMemsetAsync(p->dense, 0, sizeof(double) * (N + 1) * ld, st));
-        DPV_TSTART("dense_scatter", st);
-        k_dense_scatter<<<grid_for(p->W * 36, 256), 256, 0, st>>>(
-            p->W, p->key_a, p->key_b, p->pose_blocks, p->schur_blocks, lam, p->dense, ld,
-            p->perm_pos);
-        DPV_CHECK_LAUNCH();
-        DPV_TSTART("dense_pin_rhs", st);
-        k_dense_pin_rhs<<<grid_for(N, 256), 256, 0, st>>>(N, p->rhs_pose, p->rhs_schur, lam,
-                                                           p->scal, p->dense, ld, p->perm_pos);
-        DPV_CHECK_LAUNCH();
-        DPV_TRY(dense_factor_solve(p->dense, ld, N, status, p->red_rhs, p->bsub_part, *p->plan,
-                                   st));
-        DPV_TSTART("unpermute", st);
-        k_unpermute<<<grid_for(N, 256), 256, 0, st>>>(p->n, p->perm_pos, p->red_rhs, dp);
-        DPV_CHECK_LAUNCH();
+        DPV_TRY(dense_path(p, lam, N, *p->plan, p->perm_pos, dp, status, st));
     }
     return back_substitute(p, lam, dp, dd, st);
 }
