@@ -15,7 +15,11 @@ test_block_cholesky.py, test_geometry.py (reprojection and Jacobians vs finite
 differences), test_loop.py (global BA after closure), test_posegraph.py
 (Sim(3) pose-graph LM, residuals, Jacobians vs finite differences) and
 test_acceptance.py (the reference's acceptance criteria, minus one wall-clock
-comparison, see DESELECT).
+comparison, see DESELECT), and the callers of the path: test_graph.py and
+test_synthetic.py (edge construction / flow oracle reprojection),
+test_pipeline.py (the whole SLAM pipeline: window BA, loop closure, global
+BA and Sim(3) PGO through the shim) and test_drift.py.  Every module but
+test_trajectory.py (no hot-path call) of the reference's suite runs here.
 """
 
 import json
@@ -39,7 +43,8 @@ if not os.path.isdir(os.path.join(REF, "patchslam")) or not os.path.isdir(REF_TE
                 allow_module_level=True)
 
 MODULES = ["test_ba.py", "test_block_cholesky.py", "test_geometry.py", "test_loop.py",
-           "test_posegraph.py", "test_acceptance.py"]
+           "test_posegraph.py", "test_acceptance.py", "test_graph.py", "test_synthetic.py",
+           "test_pipeline.py", "test_drift.py"]
 # test_acceptance.py::test_criterion_03_backend_timing_direction asserts a
 # wall-clock ordering between the reference's two CPU solvers (block-sparse
 # faster than dense at 320 / 500 poses, dense no slower at 10 / 20).  On the
