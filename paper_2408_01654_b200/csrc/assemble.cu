@@ -394,6 +394,19 @@ __device__ __forceinline__ void cp_async_wait1() {
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
 }
 
+// 1/x for a positive normal x without __drcp_rn's special-case branch: the
+// library call's slow-path test splits the unrolled 9-cell loop of the edge
+// pass into ~10 basic blocks the scheduler cannot interleave.  MUFU seed +
+// two Newton steps (within 1 ulp of the correctly rounded reciprocal).
+__device__ __forceinline__ double rcp_pos(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 struct EdgeItem {
     int64_t s;        // segment (>= S: none)
     int32_t e0, e1;   // this item's edge range
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
         const double* b = ring + buf * kStgDoubles;
         const int32_t e = cur.e0 + lane;
         if (e < cur.e1) {
-            const double id = __drcp_rn(b[38 * 32 + lane]);
+            const double id = rcp_pos(b[38 * 32 + lane]);
             const double w0 = b[36 * 32 + lane], w1 = b[37 * 32 + lane];
             double ep[6] = {0, 0, 0, 0, 0, 0};
             double cdd = 0.0, gd = 0.0;
@@ -529,7 +542,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
                     xt[a] = xr[a] + uu[a];
                 }
                 const bool valid = xt[2] > kDepthEps;
-                const double iz = __drcp_rn(valid ? xt[2] : 1.0);
+                const double iz = rcp_pos(valid ? xt[2] : 1.0);
                 const double t0 = xt[0] * iz, t1 = xt[1] * iz;
                 const double p0 = fx * iz, p1 = fy * iz;
                 const double q0 = -p0 * t0, q1 = -p1 * t1;
