@@ -921,11 +921,6 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
         k_lower_bounds<int32_t><<<grid_for(NPD + 1, B), B, 0, st>>>(NPD, rows_sorted, I,
                                                                      P->rinc_ptr);
         DPV_CHECK_LAUNCH();
-        DPV_TRY(P->alloc(&P->rinc_var, I));
-        if (I > 0) {
-            k_gather_i32<<<grid_for(I, B), B, 0, st>>>(I, P->rinc, P->inc_var, P->rinc_var);
-            DPV_CHECK_LAUNCH();
-        }
     }
 
     ptimer.lap("before 9. Schur pairs per r");

@@ -106,7 +106,6 @@ struct dpv_problem {
     int32_t* var_inc_ptr = nullptr;  // (n+1) incidence range per var
     int32_t* rinc_ptr = nullptr;   // (P+1) incidences per row (ascending var)
     int32_t* rinc = nullptr;       // (I)
-    int32_t* rinc_var = nullptr;   // (I) inc_var[rinc[k]]: one dependent load less per incidence
 
     // ---- pose-pair keys -------------------------------------------------------
     int64_t* union_keys = nullptr; // (W) a*n+b, a<=b

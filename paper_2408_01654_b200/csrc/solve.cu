@@ -390,7 +390,7 @@ __global__ void k_copy_row(const double* src, int64_t n, double* dst) {
 // depth back-substitution (ba.py:321-325) and retraction (ba.py:521-531)
 
 __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
-                                  const int32_t* rinc_var, const double* inc_block,
+                                  const int32_t* inc_var, const double* inc_block,
                                   const double* rhs_depth, const double* depth_diag,
                                   const uint8_t* active, double lam, const double* dp,
                                   double* dd) {
@@ -403,8 +403,8 @@ __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int3
             const int32_t ia = __ldg(rinc + k), ib = __ldg(rinc + k + 1);
             const double* ba = inc_block + (int64_t)ia * 6;
             const double* bb = inc_block + (int64_t)ib * 6;
-            const double* xa = dp + (int64_t)__ldg(rinc_var + k) * 6;
-            const double* xb = dp + (int64_t)__ldg(rinc_var + k + 1) * 6;
+            const double* xa = dp + (int64_t)__ldg(inc_var + ia) * 6;
+            const double* xb = dp + (int64_t)__ldg(inc_var + ib) * 6;
             double va[6], vb[6], wa[6], wb[6];
 #pragma unroll
             for (int a = 0; a < 6; ++a) {
@@ -425,7 +425,7 @@ __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int3
         if (k < k1) {
             const int32_t i = rinc[k];
             const double* blk = inc_block + (int64_t)i * 6;
-            const double* x = dp + (int64_t)rinc_var[k] * 6;
+            const double* x = dp + (int64_t)inc_var[i] * 6;
             double s = 0.0;
 #pragma unroll
             for (int a = 0; a < 6; ++a) s += blk[a] * x[a];
@@ -438,7 +438,7 @@ __global__ void k_back_substitute(int64_t P, const int32_t* rinc_ptr, const int3
 
 // small problems: one warp per row, lanes over the row's incidences
 __global__ void k_back_substitute_warp(int64_t P, const int32_t* rinc_ptr, const int32_t* rinc,
-                                       const int32_t* rinc_var, const double* inc_block,
+                                       const int32_t* inc_var, const double* inc_block,
                                        const double* rhs_depth, const double* depth_diag,
                                        const uint8_t* active, double lam, const double* dp,
                                        double* dd) {
@@ -450,7 +450,7 @@ __global__ void k_back_substitute_warp(int64_t P, const int32_t* rinc_ptr, const
         for (int32_t k = rinc_ptr[r] + lane; k < rinc_ptr[r + 1]; k += 32) {
             const int32_t i = __ldg(rinc + k);
             const double* blk = inc_block + (int64_t)i * 6;
-            const double* x = dp + (int64_t)__ldg(rinc_var + k) * 6;
+            const double* x = dp + (int64_t)__ldg(inc_var + i) * 6;
             double s = 0.0;
 #pragma unroll
             for (int a = 0; a < 6; ++a) s += __ldg(blk + a) * __ldg(x + a);
@@ -764,11 +764,11 @@ int32_t back_substitute(dpv_problem* p, double lam, const double* dp, double* dd
     DPV_TSTART("back_substitute", st);
     if (p->P < (int64_t)sm_count() * 64)   // few rows: a warp each (cfg3: 0.19 vs 0.07 ms)
         k_back_substitute_warp<<<grid_for(p->P * 32, 256), 256, 0, st>>>(
-            p->P, p->rinc_ptr, p->rinc, p->rinc_var, p->inc_block, p->rhs_depth, p->depth_diag,
+            p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
             p->active, lam, dp, dd);
     else
         k_back_substitute<<<grid_for(p->P, 256), 256, 0, st>>>(
-            p->P, p->rinc_ptr, p->rinc, p->rinc_var, p->inc_block, p->rhs_depth, p->depth_diag,
+            p->P, p->rinc_ptr, p->rinc, p->inc_var, p->inc_block, p->rhs_depth, p->depth_diag,
             p->active, lam, dp, dd);
     DPV_CHECK_LAUNCH();
     return DPV_OK;
