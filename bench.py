@@ -331,15 +331,11 @@ class Stepper:
                 self.ev_join.record()
         # K1 forks after the assembly, so it overlaps the latency-bound sparse
         # factorisation rather than the bandwidth-bound assembly kernels
-        # (3.22 -> 3.13 ms per step; DPV_BENCH_CORR_AT=start: fork first)
-        late = os.environ.get("DPV_BENCH_CORR_AT", "solve") == "solve"
-        if not late:
-            k1()
+        # (measured: 3.22 -> 3.13 ms per step against forking first)
         L.check(lib.dpv_assemble_rest(self.h, P(t), s), "assemble_rest")
         if w["sharded"]:
             w["prob"].allreduce_system()      # one packed all-reduce, no host sync
-        if late:
-            k1()
+        k1()
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
                 "solve")
         L.check(lib.dpv_apply_step(self.h, P(q), P(t), P(d), P(self.dp), P(self.dd), P(q2),
@@ -560,10 +556,6 @@ def run_ours(args):
             tdist.init_process_group(args.dist_backend)
     else:
         torch.cuda.set_device(0)
-    if os.environ.get("DPV_BENCH_HIPRIO") == "1":
-        # BA chain on a high-priority stream: blocks of the side-stream K1
-        # yield SMs to it as they retire
-        torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK))
     progress("build workload")
