@@ -349,8 +349,9 @@ __device__ __forceinline__ int utri(int a, int b) {  // a <= b < 6
 // (ba.py:355-366); values agree with the world-frame pass to rounding.
 template <int Z>
 __device__ __forceinline__ void gram_row(const double (&k)[6], double wv, double rr, double jd,
-                                         double (&H)[21], double (&G)[6], double (&ep)[6],
-                                         double& cdd, double& gd, double& fobj) {
+                                         double (&acc)[28], double (&ep)[6], double& cdd,
+                                         double& gd) {
+    // acc: 0..20 Sum w k k^T (upper, utri order), 21..26 Sum w k r, 27 objective
     double wk[6];
 #pragma unroll
     for (int a = 0; a < 6; ++a) wk[a] = (a == Z) ? 0.0 : k[a] * wv;
@@ -360,15 +361,15 @@ __device__ __forceinline__ void gram_row(const double (&k)[6], double wv, double
 #pragma unroll
         for (int b = a; b < 6; ++b) {
             if (b == Z) continue;
-            H[utri(a, b)] += wk[a] * k[b];
+            acc[utri(a, b)] += wk[a] * k[b];
         }
-        G[a] += wk[a] * rr;
+        acc[21 + a] += wk[a] * rr;
         ep[a] += wk[a] * jd;
     }
     const double wjd = jd * wv;
     cdd += wjd * jd;
     gd += wjd * rr;
-    fobj += wv * rr * rr;
+    acc[27] += wv * rr * rr;
 }
 
 // The local-frame edge pass with its inputs staged through shared memory:
@@ -379,7 +380,8 @@ __device__ __forceinline__ void gram_row(const double (&k)[6], double wv, double
 // into items of <= 32 edges; the Gram sums run across a segment's items and
 // are reduced / rotated to world coordinates after its last item.
 constexpr int kStgVals = 39;                  // 18 targets, 18 rays, 2 weights, depth
-constexpr int kStgDoubles = kStgVals * 32;
+constexpr int kStgFrames = kStgVals * 32;     // + the segment's two frames (24) when it starts
+constexpr int kStgDoubles = kStgVals * 32 + 32;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
@@ -407,11 +409,33 @@ __device__ __forceinline__ double rcp_pos(double x) {
     return fma(y, e, y);
 }
 
+// a segment's bounds and frames, loaded one segment ahead of its first item
+struct SegDesc {
+    int64_t s;        // >= S: none
+    int32_t e0, se1, fs, fd;
+};
+
 struct EdgeItem {
     int64_t s;        // segment (>= S: none)
     int32_t e0, e1;   // this item's edge range
     int32_t se1;      // segment end
+    int32_t fs, fd;   // source / target frame (first item only)
+    bool first;       // first item of its segment
 };
+
+// Warp reduce-scatter of 32 per-lane values (recursive halving: 31 shuffles
+// instead of 5 per value): afterwards v[0] of lane l is the warp total of
+// value l.  Fixed tree, so the sums are reproducible run to run.
+template <int O>
+__device__ __forceinline__ void halve(double (&v)[32], int lane) {
+    const bool up = lane & O;
+#pragma unroll
+    for (int i = 0; i < O; ++i) {
+        const double send = up ? v[i] : v[i + O];
+        const double keep = up ? v[i + O] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+}
 
 template <int NW, int MINB>
 __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
@@ -440,16 +464,34 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
     double* Hs = fr + 40;
     double* Gs = fr + 76;
 
-    auto first_item = [&](int64_t s) {
-        EdgeItem it;
-        it.s = s;
+    // Segment descriptors are loaded a whole segment ahead and items two
+    // items ahead, so no global load sits on the dependency chain of an item
+    // (the per-segment seg_ptr -> a_row and seg_src -> frame chains were the
+    // kernel's long-scoreboard stalls).
+    auto load_seg = [&](int64_t s) {
+        SegDesc g;
+        g.s = s;
         if (s < S) {
-            it.e0 = seg_ptr[s];
-            it.se1 = seg_ptr[s + 1];
-            it.e1 = min(it.e0 + 32, it.se1);
+            g.e0 = __ldg(seg_ptr + s);
+            g.se1 = __ldg(seg_ptr + s + 1);
+            g.fs = __ldg(seg_src + s);
+            g.fd = __ldg(seg_dst + s);
         } else {
-            it.e0 = it.e1 = it.se1 = 0;
+            g.e0 = g.se1 = g.fs = g.fd = 0;
         }
+        return g;
+    };
+    SegDesc pend = load_seg(warp);
+    auto start_item = [&]() {
+        EdgeItem it;
+        it.s = pend.s;
+        it.e0 = pend.e0;
+        it.se1 = pend.se1;
+        it.e1 = min(it.e0 + 32, it.se1);
+        it.fs = pend.fs;
+        it.fd = pend.fd;
+        it.first = true;
+        if (pend.s < S) pend = load_seg(pend.s + nwarps);
         return it;
     };
     auto next_item = [&](const EdgeItem& it) {
@@ -457,9 +499,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
             EdgeItem n = it;
             n.e0 = it.e1;
             n.e1 = min(n.e0 + 32, it.se1);
+            n.first = false;
             return n;
         }
-        return first_item(it.s + nwarps);
+        return start_item();
     };
     auto row_of = [&](const EdgeItem& it) -> int32_t {
         const int32_t e = it.e0 + lane;
@@ -477,37 +520,37 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
             cp_async8(b + 37 * 32 + lane, a_w + E + e);
             cp_async8(b + 38 * 32 + lane, d + row);
         }
+        if (it.s < S && it.first && lane < 24) {
+            const double* src = lane < 9    ? Rall + 9 * it.fs + lane
+                                : lane < 12 ? tall + 3 * it.fs + lane - 9
+                                : lane < 21 ? Rall + 9 * it.fd + lane - 12
+                                            : tall + 3 * it.fd + lane - 21;
+            cp_async8(b + kStgFrames + lane, src);
+        }
         cp_async_commit();
     };
 
-    EdgeItem cur = first_item(warp);
+    EdgeItem cur = start_item();
     EdgeItem nx = next_item(cur);
     int32_t row_cur = row_of(cur);
     int32_t row_nx = row_of(nx);
     issue(cur, row_cur, ring);
-    double H[21], G[6];
-    double fobj = 0.0;
+    double acc[28];                   // per-lane Gram sums of the segment (gram_row)
     int buf = 0;
     while (cur.s < S) {
         // stage the next item, load the rows of the one after
         const EdgeItem nx2 = next_item(nx);
         const int32_t row_nx2 = row_of(nx2);
         issue(nx, row_nx, ring + (buf ^ 1) * kStgDoubles);
-        const bool seg_first = cur.e0 == seg_ptr[cur.s];
-        if (seg_first) {
-            __syncwarp();
-            if (lane < 12) {
-                const int32_t f = seg_src[cur.s];
-                fr[lane] = lane < 9 ? __ldg(Rall + 9 * f + lane) : __ldg(tall + 3 * f + lane - 9);
-            } else if (lane < 24) {
-                const int32_t f = seg_dst[cur.s];
-                fr[lane] = lane < 21 ? __ldg(Rall + 9 * f + lane - 12)
-                                     : __ldg(tall + 3 * f + lane - 21);
-            }
+        cp_async_wait1();
+        __syncwarp();
+        const double* b = ring + buf * kStgDoubles;
+        if (cur.first) {
+            if (lane < 24) fr[lane] = b[kStgFrames + lane];
             __syncwarp();
             if (lane < 9) {
-                const int a = lane / 3, b = lane % 3;
-                fr[24 + lane] = Rj[a] * Ri[b] + Rj[3 + a] * Ri[3 + b] + Rj[6 + a] * Ri[6 + b];
+                const int a = lane / 3, bb = lane % 3;
+                fr[24 + lane] = Rj[a] * Ri[bb] + Rj[3 + a] * Ri[3 + bb] + Rj[6 + a] * Ri[6 + bb];
             } else if (lane < 12) {
                 const int a = lane - 9;
                 fr[24 + lane] = Rj[a] * (ti[0] - tj[0]) + Rj[3 + a] * (ti[1] - tj[1]) +
@@ -517,14 +560,9 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
                 fr[24 + lane] = Rj[a] * tj[0] + Rj[3 + a] * tj[1] + Rj[6 + a] * tj[2];
             }
 #pragma unroll
-            for (int k = 0; k < 21; ++k) H[k] = 0.0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) G[k] = 0.0;
-            fobj = 0.0;
+            for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+            __syncwarp();
         }
-        cp_async_wait1();
-        __syncwarp();
-        const double* b = ring + buf * kStgDoubles;
         const int32_t e = cur.e0 + lane;
         if (e < cur.e1) {
             const double id = rcp_pos(b[38 * 32 + lane]);
@@ -553,8 +591,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
                 const double jd1 = -(p1 * xr[1] + q1 * xr[2]) * id;
                 const double r0 = (fx * t0 + cx) - b[(2 * c) * 32 + lane];
                 const double r1 = (fy * t1 + cy) - b[(2 * c + 1) * 32 + lane];
-                gram_row<1>(k0, valid ? w0 : 0.0, r0, jd0, H, G, ep, cdd, gd, fobj);
-                gram_row<0>(k1, valid ? w1 : 0.0, r1, jd1, H, G, ep, cdd, gd, fobj);
+                gram_row<1>(k0, valid ? w0 : 0.0, r0, jd0, acc, ep, cdd, gd);
+                gram_row<0>(k1, valid ? w1 : 0.0, r1, jd1, acc, ep, cdd, gd);
             }
             double ew[6];
 #pragma unroll
@@ -571,25 +609,25 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_assemble_edges_stg(
         }
         if (cur.e1 == cur.se1) {          // segment done: reduce, rotate, write
             const int64_t sg = cur.s;
+            __syncwarp();
+            double v[32];
 #pragma unroll
-            for (int k = 0; k < 21; ++k) H[k] = warp_sum(H[k]);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) G[k] = warp_sum(G[k]);
-            fobj = warp_sum(fobj);
-            if (seg_obj && lane == 0) seg_obj[sg] = fobj;
-            for (int idx = lane; idx < 36; idx += 32) {
-                const int a = idx / 6, bb = idx % 6;
-                const int t = a <= bb ? utri(a, bb) : utri(bb, a);
-                double v = 0.0;
-#pragma unroll
-                for (int q = 0; q < 21; ++q) v = (q == t) ? H[q] : v;
-                Hs[idx] = v;
-            }
-            if (lane < 6) {
-                double v = 0.0;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) v = (lane == k) ? G[k] : v;
-                Gs[lane] = v;
+            for (int k = 0; k < 32; ++k) v[k] = k < 28 ? acc[k] : 0.0;
+            halve<16>(v, lane);
+            halve<8>(v, lane);
+            halve<4>(v, lane);
+            halve<2>(v, lane);
+            halve<1>(v, lane);
+            if (lane < 21) {
+                int a = 0;
+                while (a < 5 && utri(a + 1, a + 1) <= lane) ++a;
+                const int bb = a + (lane - utri(a, a));
+                Hs[a * 6 + bb] = v[0];
+                Hs[bb * 6 + a] = v[0];
+            } else if (lane < 27) {
+                Gs[lane - 21] = v[0];
+            } else if (lane == 27 && seg_obj) {
+                seg_obj[sg] = v[0];
             }
             __syncwarp();
             if (lane < 21) {
@@ -1170,7 +1208,7 @@ int32_t assemble_edges_pass(dpv_problem* p, const double* q, const double* t, co
     if (p->S > 0) {
         DPV_ARG(p->m == 9, "assembly kernel is instantiated for 3x3 patches");
         // persistent: every warp walks many segments so the staging pipeline
-        // stays full; 4 warps x 2 blocks per SM (198 registers): 0.64 ms at
+        // stays full; 4 warps x 2 blocks per SM (225 registers): 0.50 ms at
         // cfg3 (register-capped 3x3 / 2x5 / 1x10 shapes spill: 0.83-0.86 ms)
         constexpr int kNW = 4, kMinB = 2;
         const size_t smem = sizeof(double) * 2 * kStgDoubles * kNW;
