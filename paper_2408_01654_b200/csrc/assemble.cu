@@ -832,26 +832,38 @@ __global__ void __launch_bounds__(128, MINB) k_key_blocks(
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t w = warp; w < W; w += nwarps) {
-        double h[21];
+        // lane q < 21 sums upper entry q over the key's segments in segment
+        // order (most keys have two segments, i->j and j->i; a frame's
+        // diagonal key ~2x the odometry radius), 4 loads in flight, and
+        // writes it and its mirror: no cross-lane reduction
+        {
+            const int32_t k0 = key_seg_ptr[w], k1 = key_seg_ptr[w + 1];
+            const int q = lane;
+            double hq = 0.0;
+            int32_t k = k0;
+            for (; k + 4 <= k1; k += 4) {
+                double v[4];
 #pragma unroll
-        for (int k = 0; k < 21; ++k) h[k] = 0.0;
-        for (int32_t k = key_seg_ptr[w] + lane; k < key_seg_ptr[w + 1]; k += 32) {
-            const int32_t code = key_seg[k];
-            const double sgn = (code & 1) ? -1.0 : 1.0;
-            const double* src = seg_h + (int64_t)(code >> 1) * 21;
+                for (int u = 0; u < 4; ++u) {
+                    const int32_t code = __ldg(key_seg + k + u);
+                    const double x = lane < 21 ? __ldg(seg_h + (int64_t)(code >> 1) * 21 + q) : 0.0;
+                    v[u] = (code & 1) ? -x : x;
+                }
 #pragma unroll
-            for (int q = 0; q < 21; ++q) h[q] += sgn * src[q];
-        }
-#pragma unroll
-        for (int q = 0; q < 21; ++q) h[q] = warp_sum(h[q]);
-        // lane j writes entries j and j+32 of the symmetric 6x6
-        for (int idx = lane; idx < 36; idx += 32) {
-            const int a = idx / 6, b = idx % 6;
-            const int t = a <= b ? utri(a, b) : utri(b, a);
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < 21; ++q) v = (q == t) ? h[q] : v;
-            pose_blocks[w * 36 + idx] = v;
+                for (int u = 0; u < 4; ++u) hq += v[u];
+            }
+            for (; k < k1; ++k) {
+                const int32_t code = __ldg(key_seg + k);
+                const double x = lane < 21 ? __ldg(seg_h + (int64_t)(code >> 1) * 21 + q) : 0.0;
+                hq += (code & 1) ? -x : x;
+            }
+            if (lane < 21) {
+                int a = 0;
+                while (a < 5 && utri(a + 1, a + 1) <= lane) ++a;
+                const int b = a + (lane - utri(a, a));
+                pose_blocks[w * 36 + a * 6 + b] = hq;
+                if (a != b) pose_blocks[w * 36 + b * 6 + a] = hq;
+            }
         }
         if (pose_only) continue;
         // Schur block = U^T V over the key's pair runs (l+t, r+t) on the FP64
