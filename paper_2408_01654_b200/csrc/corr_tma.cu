@@ -31,7 +31,6 @@ constexpr int kWin = 10;                  // window side (taps)
 constexpr int kTapsPad = 104;             // 13 n-tiles of 8
 constexpr int kHalfBytes = kTapsPad * 128;   // one 64-channel half of the window (swizzled rows)
 constexpr int kGHalfBytes = 16 * 128;     // 16 feature rows x 64 channels
-constexpr int kStages = 3;
 constexpr int kConsumers = 128;
 
 struct CellMeta {
@@ -85,16 +84,6 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
         "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void bar_consumers() {
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory");
-}
-
-// 128B swizzle: 16-byte chunk index XOR (row % 8) inside each 1024-byte atom
-__device__ __forceinline__ uint32_t ld_sw(const unsigned char* base, int row, int ch) {
-    return *reinterpret_cast<const uint32_t*>(base + row * 128 + ((((ch >> 3) ^ row) & 7) << 4) +
-                                              (ch & 7) * 2);
-}
-
 // four 8x8 b16 matrices from shared memory; lane l addresses row l % 8 of
 // matrix l / 8 (16 contiguous bytes = one swizzle chunk)
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], unsigned addr) {

@@ -21,7 +21,6 @@ namespace dpv {
 namespace {
 
 constexpr int kSmallMax = 162;    // n <= 27 poses: single-CTA shared-memory solve
-constexpr int kTile = 64;         // SYRK output tile
 
 // S(lam) block value at entry (i, j) of key w (ba.py:305-309)
 __device__ __forceinline__ double reduced_entry(const double* pose, const double* schur,
@@ -117,35 +116,6 @@ __global__ void k_unpermute(int64_t n, const int32_t* pos, const double* x, doub
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < 6 * n;
          c += (int64_t)gridDim.x * blockDim.x)
         dp[c] = x[6 * (int64_t)pos[c / 6] + c % 6];
-}
-
-// ---------------------------------------------------------------------------
-// in-shared-memory factor of an nb x nb lower block (right-looking).  Returns
-// through *bad the first non-positive pivot (LAPACK potrf semantics).
-
-__device__ void smem_potrf(double* L, int ldl, int nb, int* bad, int pivot_base,
-                           int* status) {
-    for (int j = 0; j < nb; ++j) {
-        if (threadIdx.x == 0) {
-            double piv = L[j * ldl + j];
-            if (!(piv > 0.0)) {
-                if (*bad < 0) *bad = pivot_base + j;
-                piv = 1.0;
-            }
-            L[j * ldl + j] = sqrt(piv);
-        }
-        __syncthreads();
-        const double ljj = L[j * ldl + j];
-        for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) L[i * ldl + j] /= ljj;
-        __syncthreads();
-        const int rem = nb - j - 1;
-        for (int x = threadIdx.x; x < rem * rem; x += blockDim.x) {
-            const int i = j + 1 + x / rem, k = j + 1 + x % rem;
-            if (k <= i) L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j];
-        }
-        __syncthreads();
-    }
-    (void)status;
 }
 
 // ---------------------------------------------------------------------------
@@ -378,12 +348,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_solve2(
     for (int c = tid; c < N; c += kSmallThreads) dp[c] = xs[c];
     if (tid == 0) status[0] = bad >= 0 ? 1 : 0;
     if (tid == 0) status[1] = bad;
-}
-
-__global__ void k_copy_row(const double* src, int64_t n, double* dst) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------------------
