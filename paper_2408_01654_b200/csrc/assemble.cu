@@ -938,49 +938,55 @@ __global__ void __launch_bounds__(256) k_group_syrk(const int4* __restrict__ chu
 #pragma unroll
         for (int c = 0; c < 6; ++c) Ws[(6 * j + c) * ldt + t] = v[c];
     }
-    for (int x = tid; x < (8 * TR - n6) * ldt; x += blockDim.x) Ws[n6 * ldt + x] = 0.0;
+    // zero rows up to a whole 2 x 2 block of tiles (16 rows)
+    const int TB2 = (TR + 1) / 2;
+    for (int x = tid; x < (16 * TB2 - n6) * ldt; x += blockDim.x) Ws[n6 * ldt + x] = 0.0;
     __syncthreads();
-    const int nt = TR * (TR + 1) / 2;
+    // upper triangle of 2 x 2 blocks of 8 x 8 tiles, one block per warp and
+    // round: 4 operand loads feed 4 DMMAs (the 1 x 2 form was bound by the
+    // shared-memory operand loads, 4 per 2 DMMAs)
+    const int nb = TB2 * (TB2 + 1) / 2;
     const int lr = lane >> 2, lc = lane & 3;
     const int kend = (nr + 3) & ~3;
-    for (int q0 = warp * 2; q0 < nt; q0 += 16) {
-        int tt[2][2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            int q = min(q0 + u, nt - 1), t1 = 0;
-            while (q >= TR - t1) {
-                q -= TR - t1;
-                ++t1;
-            }
-            tt[u][0] = t1;
-            tt[u][1] = t1 + q;
+    for (int q = warp; q < nb; q += 8) {
+        int bi = 0, rem = q;
+        while (rem >= TB2 - bi) {
+            rem -= TB2 - bi;
+            ++bi;
         }
-        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        const double* a0 = Ws + (8 * tt[0][0] + lr) * ldt + lc;
-        const double* b0 = Ws + (8 * tt[0][1] + lr) * ldt + lc;
-        const double* a1 = Ws + (8 * tt[1][0] + lr) * ldt + lc;
-        const double* b1 = Ws + (8 * tt[1][1] + lr) * ldt + lc;
+        const int bj = bi + rem;
+        double c[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+        const double* a0 = Ws + (16 * bi + lr) * ldt + lc;
+        const double* a1 = a0 + 8 * ldt;
+        const double* b0 = Ws + (16 * bj + lr) * ldt + lc;
+        const double* b1 = b0 + 8 * ldt;
 #pragma unroll 4
         for (int k = 0; k < kend; k += 4) {
-            dmma_f64(c[0][0], c[0][1], a0[k], b0[k]);
-            dmma_f64(c[1][0], c[1][1], a1[k], b1[k]);
+            const double x0 = a0[k], x1 = a1[k], y0 = b0[k], y1 = b1[k];
+            dmma_f64(c[0][0][0], c[0][0][1], x0, y0);
+            dmma_f64(c[0][1][0], c[0][1][1], x0, y1);
+            dmma_f64(c[1][0][0], c[1][0][1], x1, y0);
+            dmma_f64(c[1][1][0], c[1][1][1], x1, y1);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (q0 + u >= nt) break;
-            const int r = 8 * tt[u][0] + lr;
+        for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int cc = 8 * tt[u][1] + 2 * lc + h;
-                if (r >= n6 || cc >= n6) continue;
-                const int vr = r / 6, vc = cc / 6, i = r % 6, jj = cc % 6;
-                if (vr > vc) continue;              // mirror of an element of this tile
-                const int blk = vr * m - vr * (vr - 1) / 2 + (vc - vr);
-                double* dst = sbuf + ((int64_t)ch.w + blk) * 36;
-                dst[i * 6 + jj] = c[u][h];
-                if (vr == vc) dst[jj * 6 + i] = c[u][h];   // symmetric diagonal block
+            for (int v = 0; v < 2; ++v) {
+                const int tr = 2 * bi + u, tc = 2 * bj + v;
+                if (tr > tc || tc >= TR) continue;
+                const int r = 8 * tr + lr;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = 8 * tc + 2 * lc + h;
+                    if (r >= n6 || cc >= n6) continue;
+                    const int vr = r / 6, vc = cc / 6, i = r % 6, jj = cc % 6;
+                    if (vr > vc) continue;          // mirror of an element of this tile
+                    const int blk = vr * m - vr * (vr - 1) / 2 + (vc - vr);
+                    double* dst = sbuf + ((int64_t)ch.w + blk) * 36;
+                    dst[i * 6 + jj] = c[u][v][h];
+                    if (vr == vc) dst[jj * 6 + i] = c[u][v][h];   // symmetric diagonal block
+                }
             }
-        }
     }
 }
 

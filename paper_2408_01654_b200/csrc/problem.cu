@@ -1096,8 +1096,10 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
     // <= rows_per_chunk rows; each key sums its chunk blocks in a fixed order
     P->grouped = 0;
     // Opt-in (DPV_SCHUR_GROUPED=1): at cfg3 the pair-run DMMA kernel is faster
-    // (0.51 vs 0.44 + 0.1 ms: the grouped form wastes 8x8 tile work on 6-wide
-    // var blocks and its staging is a gather); it wins for dense var sets.
+    // (0.42 ms for its Schur part vs SYRK 0.37 + ordered chunk sum 0.11 ms:
+    // the SYRK's per-chunk staging is a gather it cannot overlap, and every
+    // chunk's blocks make a round trip through memory); it wins for dense
+    // var sets.
     if (NPD > 0 && getenv("DPV_SCHUR_GROUPED") && atoi(getenv("DPV_SCHUR_GROUPED")) != 0) {
         uint64_t *rh, *rh_s;
         int32_t *ridx, *flag, *gid, *bad;
@@ -1154,9 +1156,10 @@ int32_t build_problem(const dpv_graph* g, int32_t first, int32_t last, const int
                 const int32_t head = h_rows[b0];
                 const int m = h_rinc_ptr[head + 1] - h_rinc_ptr[head];
                 if (m == 0) continue;
-                // staged W: 8m rows x (rows + <=16 padding) doubles <= kSyrkSmemDoubles
+                // staged W: 6m rows + zero rows to a whole 16-row block, x (rows
+                // + <= 16 padding) doubles <= kSyrkSmemDoubles
                 const int rpc = std::min(kSyrkMaxRows,
-                                         ((int)(kSyrkSmemDoubles / (6 * m + 8)) - 16) & ~3);
+                                         ((int)(kSyrkSmemDoubles / (6 * m + 16)) - 16) & ~3);
                 if (rpc < 4) { h_bad = 1; break; }
                 for (int32_t r0 = b0; r0 < b1; r0 += rpc) {
                     chunks.push_back(make_int4(r0, std::min(rpc, b1 - r0), m, (int)nblk));
