@@ -64,8 +64,17 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batch", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="eager steps (no CUDA graph)")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as a CUDA graph (a graph replay ignores the streams' "
+                         "priorities, so K1 then delays the solve: measured 2.54 vs 2.40 ms)")
+    ap.add_argument("--no-graph", action="store_true", help="eager steps (the default)")
     ap.add_argument("--batch-seqs", type=int, default=8)
+    ap.add_argument("--corr-items", type=int, default=32,
+                    help="K1 items per CTA beside the solve (0: one persistent CTA per SM)")
+    ap.add_argument("--k1-early", action="store_true",
+                    help="fork K1 before the rest of the assembly instead of after it")
+    ap.add_argument("--no-priority", action="store_true",
+                    help="BA step on a default-priority stream (K1 then competes for SMs)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: multi-rank tests on one GPU)")
@@ -245,7 +254,13 @@ class Stepper:
         P = int(work["info"].n_depths)
         dev = "cuda"
         self.Ec = len(work["csel"])
-        self.side = torch.cuda.Stream()           # K1 runs beside the BA step
+        # K1 runs beside the BA step on a default (= lowest) priority stream
+        # in short-lived CTAs (corr_items per CTA): the BA step runs on a
+        # high-priority stream, so the block scheduler gives it SMs first and
+        # K1 fills the SMs its latency-bound solve leaves idle
+        self.side = torch.cuda.Stream()
+        self.corr_items = 0
+        self.fork_early = False
         self.overlap = True                       # False: serialise (per-kernel timing)
         self.ev_fork = torch.cuda.Event()
         self.ev_join = torch.cuda.Event()
@@ -327,15 +342,19 @@ class Stepper:
                 L.check(lib.dpv_reproject_coords_sel(self.h, P(q), P(t), P(d), 0.25,
                                                      P(w["csel"]), self.Ec, P(self.coords),
                                                      L.stream_ptr()), "coords")
-                corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout)
+                corr.corr(w["gmap"], w["pyr"], self.coords, w["ii"], w["jj"], out=self.cout,
+                          items_per_cta=self.corr_items if self.overlap else 0)
                 self.ev_join.record()
         # K1 forks after the assembly, so it overlaps the latency-bound sparse
         # factorisation rather than the bandwidth-bound assembly kernels
         # (measured: 3.22 -> 3.13 ms per step against forking first)
+        if self.fork_early:
+            k1()
         L.check(lib.dpv_assemble_rest(self.h, P(t), s), "assemble_rest")
         if w["sharded"]:
             w["prob"].allreduce_system()      # one packed all-reduce, no host sync
-        k1()
+        if not self.fork_early:
+            k1()
         L.check(lib.dpv_solve(self.h, self.lam, P(self.dp), P(self.dd), P(self.status), s),
                 "solve")
         L.check(lib.dpv_apply_step(self.h, P(q), P(t), P(d), P(self.dp), P(self.dd), P(q2),
@@ -558,10 +577,16 @@ def run_ours(args):
         torch.cuda.set_device(0)
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK))
+    if not args.no_priority:
+        # the BA step (and everything timed) on a high-priority stream; K1's
+        # side stream keeps the default, lowest priority (Stepper)
+        torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     progress("build workload")
     work = build_workload(args, torch)
     progress("workload built")
     st = Stepper(work, torch)
+    st.corr_items = args.corr_items
+    st.fork_early = args.k1_early
     # device-resident step: one LM iteration with speculative assembly (the
     # native driver's flow); the sharded path keeps assemble + NCCL + objective
     st.lm_init()
@@ -572,17 +597,20 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
-    # the device step is a fixed launch sequence: capture two steps (the state
-    # buffers swap every step, so two steps return to the starting
+    # --graph: the device step is a fixed launch sequence: capture two steps
+    # (the state buffers swap every step, so two steps return to the starting
     # assignment) as one CUDA graph and replay it; kernels are counted at
-    # capture (the library counts every launch it issues)
+    # capture (the library counts every launch it issues).  Not the default:
+    # a replayed graph ignores the stream priorities that let K1 fill the
+    # solve's idle SMs (also with per-node priorities and
+    # cudaGraphInstantiateFlagUseNodePriority: measured 2.59 vs 2.40 ms eager)
     graph = None
     per_graph = 0
-    if not work["sharded"] and not args.no_graph and args.steps % 2 == 0:
+    if not work["sharded"] and args.graph and not args.no_graph and args.steps % 2 == 0:
         try:
             graph = torch.cuda.CUDAGraph()
             l0 = _lib.lib().dpv_launch_count()
-            with torch.cuda.graph(graph):
+            with torch.cuda.graph(graph, stream=torch.cuda.current_stream()):
                 step_fn()
                 step_fn()
             per_graph = _lib.lib().dpv_launch_count() - l0
@@ -720,11 +748,16 @@ def run_ours(args):
                    "corr_levels": 2, "corr_channels": work["C"], "corr_dtype": args.feat_dtype,
                    "feature_frames": work["n_feat_frames"],
                    "lm_attempt_per_step": 1,
-                   "step_kind": ("device-only LM iteration replayed as a CUDA graph: fixed lambda, "
+                   "step_kind": ("device-only LM iteration (" + ("replayed as a CUDA graph" if graph
+                                 is not None else "eager launches") + "): fixed lambda, "
                                  "the candidate is always accepted, no host read-back; the native "
                                  "driver's per-iteration time (host accept test, lambda "
                                  "escalation) is global_ba.iteration_ms"),
                    "cuda_graph": graph is not None,
+                   "k1_overlap": ("BA step kernels at the greatest node/stream priority, K1 at "
+                                  f"the least in CTAs of {args.corr_items} items (fills the SMs "
+                                  "the latency-bound solve leaves idle)") if not args.no_priority
+                                 else "K1 persistent, default priorities",
                    "step": ("one LM iteration (speculative assembly: rest of the assembly at x, "
                             "sparse solve, retraction, edge pass at the candidate = its "
                             "objective and the next iteration's terms; state advances) + K1 "
@@ -910,7 +943,8 @@ def run_e2e_solve(work, args, torch, steps=6):
         fork.record(main)
         with torch.cuda.stream(side):
             side.wait_event(fork)
-            corr.corr(work["gmap"], work["pyr"], coords, work["ii"], work["jj"], out=cout)
+            corr.corr(work["gmap"], work["pyr"], coords, work["ii"], work["jj"], out=cout,
+                      items_per_cta=args.corr_items)
             join.record(side)
         params = _lib.DpvLmParams(args.lm_iters, 1e-9, 1e-4)
         rep = _lib.DpvLmReport()

@@ -362,6 +362,18 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
                     int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
                     void* stream);
 
+/* dpv_corr_ex with a CTA work size: items_per_cta = 0 runs one persistent
+ * CTA per SM (fastest alone); > 0 cuts each SM's share of (edge, level)
+ * items into CTAs of that many items, so when the lookup runs on a
+ * low-priority stream beside a higher-priority one (the correlation beside
+ * the BA solve) the scheduler hands SMs back at CTA granularity and the
+ * lookup fills the SMs the latency-bound solve leaves idle.  Same results. */
+int32_t dpv_corr_ex2(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                     int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                     int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
+                     int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype,
+                     int64_t items_per_cta, float* out, void* stream);
+
 /* Proximity loop-closure candidates (loop.py:64-85): centers (n_frames, 3)
  * DEVICE f64 camera centres; pairs (capacity, 2) DEVICE int64 (old, recent),
  * sorted by centre distance (ties: recent, then old ascending) exactly as the

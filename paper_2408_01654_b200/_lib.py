@@ -117,6 +117,9 @@ SIGNATURES = {
     "dpv_corr_ex": (C.c_int32, [vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, C.c_int64,
                                 C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_int32, C.c_int32, vp, vp]),
+    "dpv_corr_ex2": (C.c_int32, [vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, C.c_int64,
+                                 C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                 C.c_int32, C.c_int32, C.c_int64, vp, vp]),
 }
 
 _lib = None

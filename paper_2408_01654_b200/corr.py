@@ -32,7 +32,8 @@ def pyramid(fmap: torch.Tensor):
 
 
 def corr(gmap: torch.Tensor, fmaps, coords: torch.Tensor, ii: torch.Tensor, jj: torch.Tensor,
-         radius: int = 3, out: torch.Tensor | None = None) -> torch.Tensor:
+         radius: int = 3, out: torch.Tensor | None = None,
+         items_per_cta: int = 0) -> torch.Tensor:
     levels = len(fmaps)
     if levels not in (1, 2):
         raise ValueError("1 or 2 pyramid levels")
@@ -46,10 +47,10 @@ def corr(gmap: torch.Tensor, fmaps, coords: torch.Tensor, ii: torch.Tensor, jj: 
     f0 = fmaps[0].contiguous()
     f1 = fmaps[1].contiguous() if levels == 2 else None
     g = gmap.contiguous()
-    _lib.check(_lib.lib().dpv_corr_ex(
+    _lib.check(_lib.lib().dpv_corr_ex2(
         _lib.ptr(g), int(g.shape[0]), _lib.ptr(f0), _lib.ptr(f1), int(f0.shape[0]),
         _lib.ptr(coords.to(torch.float64).contiguous()), _lib.ptr(ii.to(torch.int32).contiguous()),
         _lib.ptr(jj.to(torch.int32).contiguous()), E, C, f0.shape[1], f0.shape[2],
         f1.shape[1] if f1 is not None else 0, f1.shape[2] if f1 is not None else 0, levels,
-        radius, _DT[gmap.dtype], _lib.ptr(out), _lib.stream_ptr()), "corr")
+        radius, _DT[gmap.dtype], int(items_per_cta), _lib.ptr(out), _lib.stream_ptr()), "corr")
     return out

@@ -886,15 +886,16 @@ int32_t dpv_corr(const void* gmap, const void* fmap0, const void* fmap1, const d
     DPV_ABI_CATCH
 }
 
-int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
-                    int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
-                    int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
-                    int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
-                    void* stream) {
+int32_t dpv_corr_ex2(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                     int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                     int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
+                     int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype,
+                     int64_t items_per_cta, float* out, void* stream) {
     DPV_ABI_TRY
     clear_error();
     DPV_ARG(n_edges >= 0 && channels > 0 && (n_levels == 1 || n_levels == 2) && radius >= 0 &&
-                radius <= 4 && (dtype == 0 || dtype == 1) && n_patches >= 0 && n_frames >= 0,
+                radius <= 4 && (dtype == 0 || dtype == 1) && n_patches >= 0 && n_frames >= 0 &&
+                items_per_cta >= 0,
             "bad corr args");
     DPV_ARG(n_edges == 0 || (gmap && fmap0 && coords && ii && jj && out), "NULL corr argument");
     DPV_ARG(n_levels == 1 || fmap1, "level-1 feature map missing");
@@ -903,13 +904,23 @@ int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, cons
     // TMA + tensor-core path: bf16, radius 3, C in {64, 128, 256}
     if (dtype == 1 && radius == 3) {
         const int32_t r = corr_tma(gmap, n_patches, fmap0, fmap1, n_frames, coords, ii, jj,
-                                   n_edges, channels, h0, w0, h1, w1, n_levels, out, st);
+                                   n_edges, channels, h0, w0, h1, w1, n_levels, out,
+                                   items_per_cta, st);
         if (r != DPV_BAD_ARGS) return r;
         clear_error();
     }
     return corr(gmap, fmap0, fmap1, coords, ii, jj, n_edges, channels, h0, w0, h1, w1, n_levels,
                 radius, dtype, out, st);
     DPV_ABI_CATCH
+}
+
+int32_t dpv_corr_ex(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
+                    int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
+                    int64_t n_edges, int32_t channels, int32_t h0, int32_t w0, int32_t h1,
+                    int32_t w1, int32_t n_levels, int32_t radius, int32_t dtype, float* out,
+                    void* stream) {
+    return dpv_corr_ex2(gmap, n_patches, fmap0, fmap1, n_frames, coords, ii, jj, n_edges, channels,
+                        h0, w0, h1, w1, n_levels, radius, dtype, 0, out, stream);
 }
 
 int32_t dpv_proximity_detect(const double* centers, int64_t n_frames, int64_t min_gap,

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
     const __nv_bfloat16* __restrict__ fmap1, const __nv_bfloat16* __restrict__ gmap,
     const double* __restrict__ coords, const int32_t* __restrict__ ii,
     const int32_t* __restrict__ jj, int64_t E, int h0, int w0, int h1, int w1, int levels,
-    float* __restrict__ out) {
+    int vgrid, int64_t chunk, float* __restrict__ out) {
     using Cfg = CorrCfg<NH>;
     constexpr int C = 64 * NH, SB = Cfg::SB, NS = Cfg::NS, NG = Cfg::NG;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -182,10 +182,18 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // grid-stride items: the CTAs work on neighbouring edges at any time, so
-    // the target frames' feature maps stay L2-resident (edges grouped by frame)
+    // grid-stride items over vgrid virtual CTAs: the CTAs work on neighbouring
+    // edges at any time, so the target frames' feature maps stay L2-resident
+    // (edges grouped by frame).  Virtual CTA vb's local items are split into
+    // chunks of `chunk`; CTA blockIdx.x runs chunk blockIdx.x / vgrid of
+    // virtual CTA blockIdx.x % vgrid (one persistent CTA per SM: vgrid =
+    // gridDim.x, one chunk).  Short-lived CTAs let a higher-priority stream
+    // take SMs back at CTA granularity (the correlation beside the solve).
     const int64_t NV = E * levels;
-    const int64_t n_my = NV > blockIdx.x ? (NV - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int vb = (int)(blockIdx.x % (unsigned)vgrid);
+    const int64_t U0 = (int64_t)(blockIdx.x / (unsigned)vgrid) * chunk;
+    const int64_t n_v = NV > vb ? (NV - vb + vgrid - 1) / vgrid : 0;
+    const int64_t n_my = n_v > U0 ? min(chunk, n_v - U0) : 0;
     constexpr int radius = 3, D = 8, O = 7;
 
     constexpr int NP = Cfg::NP;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
         auto edge_of = [&](int64_t v) { return levels == 2 ? (v >> 1) : v; };
         auto fetch = [&](int64_t i) {
             if (i >= n_mine || lg != (int)(i % kLook)) return;
-            const int64_t e = edge_of(blockIdx.x + (warp + i * NP) * (int64_t)gridDim.x);
+            const int64_t e = edge_of(vb + (U0 + warp + i * NP) * (int64_t)vgrid);
             cxr = __ldg(coords + (e * kCellsT + lc) * 2);
             cyr = __ldg(coords + (e * kCellsT + lc) * 2 + 1);
             if (lc == 0) {
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(CorrCfg<NH>::kThreadsT, DPV_CORR_CTAS) k_corr_
         for (int q = 0; q < kLook; ++q) fetch(q);
         for (int64_t i = 0; i < n_mine; ++i) {
             const int64_t u = warp + i * NP;
-            const int64_t v = blockIdx.x + u * (int64_t)gridDim.x;
+            const int64_t v = vb + (U0 + u) * (int64_t)vgrid;
             const int64_t e = edge_of(v);
             const int level = levels == 2 ? (int)(v & 1) : 0;
             const int s = (int)(u % NS);
@@ -410,7 +418,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
                  int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
                  int64_t E, int C, int h0, int w0, int h1, int w1, int levels, float* out,
-                 cudaStream_t st) {
+                 int64_t items_per_cta, cudaStream_t st) {
     auto enc = encode_fn();
     if (!enc || (C != 64 && C != 128 && C != 256) || n_patches < 1 || n_frames < 1 ||
         (levels == 2 && (!fmap1 || h1 < 1 || w1 < 1)) ||
@@ -450,14 +458,18 @@ int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap0, const v
         static size_t cur[3] = {0, 0, 0};
         DPV_TRY(ensure_smem(kern, smem, cur[slot]));
         const int64_t items = E * levels;
-        const int grid =
+        const int vgrid =
             (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sm_count() * DPV_CORR_CTAS));
+        const int64_t per = (items + vgrid - 1) / vgrid;          // local items per virtual CTA
+        const int64_t chunk = items_per_cta > 0 ? std::min(items_per_cta, per) : per;
+        const int64_t grid = (int64_t)vgrid * ((per + chunk - 1) / chunk);
+        if (grid > INT32_MAX) return DPV_BAD_ARGS;
         DPV_TSTART("corr", st);
-        kern<<<grid, threads, smem, st>>>(fm[0], fm[1], gm,
+        kern<<<(unsigned)grid, threads, smem, st>>>(fm[0], fm[1], gm,
                                           reinterpret_cast<const __nv_bfloat16*>(fmap0),
                                           reinterpret_cast<const __nv_bfloat16*>(fmap1),
                                           reinterpret_cast<const __nv_bfloat16*>(gmap), coords,
-                                          ii, jj, E, h0, w0, h1, w1, levels, out);
+                                          ii, jj, E, h0, w0, h1, w1, levels, vgrid, chunk, out);
         DPV_CHECK_LAUNCH();
         return DPV_OK;
     };

@@ -246,7 +246,7 @@ int32_t update_targets(dpv_problem* p, const double* tgt, const double* conf, cu
 int32_t corr_tma(const void* gmap, int64_t n_patches, const void* fmap0, const void* fmap1,
                  int64_t n_frames, const double* coords, const int32_t* ii, const int32_t* jj,
                  int64_t E, int C, int h0, int w0, int h1, int w1, int levels, float* out,
-                 cudaStream_t st);
+                 int64_t items_per_cta, cudaStream_t st);
 int32_t corr(const void* gmap, const void* fmap0, const void* fmap1, const double* coords,
              const int32_t* ii, const int32_t* jj, int64_t E, int C, int h0, int w0, int h1,
              int w1, int levels, int radius, int dtype, float* out, cudaStream_t st);

@@ -147,3 +147,25 @@ def test_corr_single_level_and_odd_counts():
                                coords, ii, jj)
         assert out.shape == (E, 1, 9, 7, 7)
         assert np.abs(out.cpu().numpy() - ref).max() < 2e-4
+
+
+@pytest.mark.parametrize("items", [1, 7, 48, 10_000])
+def test_corr_items_per_cta_identical(items):
+    """Short-lived CTAs (items_per_cta > 0: the lookup beside the solve on a
+    low-priority stream) compute exactly the persistent kernel's outputs,
+    including item counts that leave ragged last chunks."""
+    rng = np.random.default_rng(11 + items)
+    E = 5_003
+    g, f, coords, ii, jj = bench_shape_case(rng, E, 120, 160, F=6, P=500)
+    gd = torch.as_tensor(g, device="cuda").bfloat16()
+    pyr = corr.pyramid(torch.as_tensor(f, device="cuda").bfloat16())
+    args = (gd, pyr, torch.as_tensor(coords, device="cuda"), torch.as_tensor(ii, device="cuda"),
+            torch.as_tensor(jj, device="cuda"))
+    ref = corr.corr(*args)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        got = corr.corr(*args, items_per_cta=items)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    with pytest.raises(Exception):
+        corr.corr(*args, items_per_cta=-1)
