@@ -34,6 +34,13 @@ def pyramid(fmap: torch.Tensor):
 def corr(gmap: torch.Tensor, fmaps, coords: torch.Tensor, ii: torch.Tensor, jj: torch.Tensor,
          radius: int = 3, out: torch.Tensor | None = None,
          items_per_cta: int = 0) -> torch.Tensor:
+    """K1 for every edge at every level of ``fmaps`` (``dpv_corr_ex2``).
+
+    items_per_cta = 0 runs one persistent CTA per SM (fastest alone); > 0
+    runs short-lived CTAs of that many (edge, level) items, for a lookup on
+    a low-priority stream beside higher-priority work (bench.py runs it
+    beside the BA solve with 32): the block scheduler then gives SMs back to
+    the other stream at CTA granularity.  Results are identical."""
     levels = len(fmaps)
     if levels not in (1, 2):
         raise ValueError("1 or 2 pyramid levels")
