@@ -2,6 +2,7 @@
 // factorisation used on the solver's critical path (spd.cu potrf_inv64).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        tools/spd_micro.cu -o tools/spd_micro
+#include <cstring>
 #include "../paper_2408_01654_b200/csrc/spd.cu"
 
 namespace dpv {
@@ -108,6 +109,15 @@ int main() {
         long long b; cudaMemcpy(&b, dc, 8, cudaMemcpyDeviceToHost);
         printf("factor_block8 (1 warp): %lld cycles; barrier+lds/sts step (256 thr): %lld cycles\n", f, b);
     }
+    unsigned long long hl = 0, hx = 0;
+    for (int x = 0; x < 4096; ++x) {
+        unsigned long long u, v;
+        memcpy(&u, &L[x], 8);
+        memcpy(&v, &X[x], 8);
+        hl = hl * 1000003ull ^ u;
+        hx = hx * 1000003ull ^ v;
+    }
+    printf("bits: L %016llx X %016llx\n", hl, hx);
     printf("potrf_inv64: %lld cycles (%.2f us @1.965GHz), bad=%lld, |LL^T-A|=%.2e |XL-I|=%.2e  %s\n",
            c[0], c[0] / 1965.0, c[1], e1, e2, cudaGetErrorString(cudaDeviceSynchronize()));
 }
