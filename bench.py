@@ -740,12 +740,11 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bit-exactly; random features)",
-        "config": {"workload": f"{args.config}: {DESC.get(args.config, args.config)} + corr on "
-                               "the window/loop edges",
+        "config": workload_config(args, work["graph"], work["free"], world),
+        "workload_stats": {
                    "E_ba": work["E"], "E_corr": len(work["csel"]),
                    "P": int(work["info"].n_depths), "n_free": int(work["info"].n_free),
                    "W_blocks": int(work["info"].n_keys), "pairs": int(work["info"].n_pairs),
-                   "corr_levels": 2, "corr_channels": work["C"], "corr_dtype": args.feat_dtype,
                    "feature_frames": work["n_feat_frames"],
                    "lm_attempt_per_step": 1,
                    "step_kind": ("device-only LM iteration (" + ("replayed as a CUDA graph" if graph
@@ -765,12 +764,7 @@ def run_ours(args):
                            ("one LM iteration on this rank's edge shard: rest of the assembly, "
                             "all-reduce of the reduced pose system, redundant sparse solve, "
                             "retraction, edge pass at the candidate + all-reduce of its "
-                            "objective; K1 beside it"),
-                   "parallelism": (f"edge-shard x{world} by depth row, one "
-                                   f"{args.dist_backend.upper()} all-reduce of the packed reduced "
-                                   "pose system per step" if world > 1 else "single GPU"),
-                   "l2": f"inputs larger than L2 (flow targets {work['E'] * 144 / 1e9:.2f} GB, "
-                         "126 MB L2)"},
+                            "objective; K1 beside it")},
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernels": kernels,
@@ -1242,6 +1236,24 @@ def run_global(work, args, torch):
             "includes": "BAProblem index build + native LM + write-back"}
 
 
+def workload_config(args, graph, free, world):
+    """The bench line's `config`: the workload named from host data only, so
+    the reference arm (which runs a bounded sample of it on the CPU and
+    describes the sample in cpu_baseline.sample) prints the same dict."""
+    from paper_2408_01654_b200.synthetic import DESCRIPTIONS as DESC
+    return {"workload": f"{args.config}: {DESC.get(args.config, args.config)} + corr on "
+                        "the window/loop edges",
+            "frames": int(graph.n_frames), "patches": int(graph.n_patches),
+            "graph_edges": int(graph.n_edges), "free_poses": [int(free[0]), int(free[1])],
+            "corr_window": args.window, "corr_levels": 2, "corr_channels": args.channels,
+            "corr_dtype": args.feat_dtype,
+            "parallelism": (f"edge-shard x{world} by depth row, one "
+                            f"{args.dist_backend.upper()} all-reduce of the packed reduced "
+                            "pose system per step" if world > 1 else "single GPU"),
+            "l2": f"inputs larger than L2 (flow targets {graph.n_edges * 144 / 1e9:.2f} GB, "
+                  "126 MB L2)"}
+
+
 def run_reference(args):
     """Reference arm: the unmodified reference package (baseline/_ref) on the
     host cores -- each step one full LM iteration of the named sub-problem of
@@ -1272,8 +1284,9 @@ def run_reference(args):
         "warmup": warm, "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bit-exactly)",
-        "config": {"workload": (f"{args.config} graph, global BA over its first {prefix} frames "
-                                f"(the bounded sample; the ours arm runs all {graph.n_frames})"),
+        "config": workload_config(args, graph, free, int(os.environ.get("WORLD_SIZE", "1"))),
+        "sample": {"workload": (f"{args.config} graph, global BA over its first {prefix} frames "
+                                f"(the bounded sample of the ours arm's {graph.n_frames})"),
                    "E_ba": r["E"], "E_corr": 0,
                    "corr": "none: the reference has no correlation code (SPEC.md:14)"},
         "cpu_baseline": {"value": value, "unit": "patch-edges/s", "cores": r["cores"],
