@@ -132,15 +132,25 @@ class ClockSampler:
             self.nvml = None
         return self
 
-    def _poll(self):
+    def sample(self):
+        """One NVML reading (also called from the launching thread between
+        eager steps, so the timed region is covered even when the polling
+        thread is starved of the GIL)."""
         p = self.nvml
+        if p is None:
+            return
+        try:
+            sm = p.nvmlDeviceGetClockInfo(self.handle, p.NVML_CLOCK_SM)
+            rs = p.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+            self.rows.append((sm, rs, time.perf_counter()))
+        except Exception:
+            self.errors += 1
+
+    errors = 0
+
+    def _poll(self):
         while not self.stop.is_set():
-            try:
-                sm = p.nvmlDeviceGetClockInfo(self.handle, p.NVML_CLOCK_SM)
-                rs = p.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-                self.rows.append((sm, rs, time.perf_counter()))
-            except Exception:
-                pass
+            self.sample()
             time.sleep(0.001)
 
     # the thread is started (NVML initialised) before the warm-up; only the
@@ -164,7 +174,8 @@ class ClockSampler:
         if self.t0 is not None and self.t1 is not None:
             rows = [r for r in rows if self.t0 <= r[2] <= self.t1]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0,
+                    "nvml_errors": self.errors}
         p = self.nvml
         reasons = sorted({name for _, rs, _ in rows for name, attr in self.NAMES
                           if hasattr(p, attr) and rs & getattr(p, attr)})
@@ -367,13 +378,15 @@ class Stepper:
         torch.cuda.current_stream().wait_event(self.ev_join)
 
 
-def time_steps(fn, k, torch):
+def time_steps(fn, k, torch, clk=None):
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(k):
         fn()
+        if clk is not None:          # the device runs ahead of the launching thread
+            clk.sample()
     b.record()
     # wait with the GIL released so the clock sampler thread keeps polling
     # while the device runs (graph replays return immediately)
@@ -627,7 +640,7 @@ def run_ours(args):
     if graph is not None:
         ms = time_steps(graph.replay, args.steps // 2, torch)
     else:
-        ms = time_steps(step_fn, args.steps, torch)
+        ms = time_steps(step_fn, args.steps, torch, clk)
     clk.mark_end()
     clk.__exit__(None, None, None)
     launches = _lib.lib().dpv_launch_count() - launches0
