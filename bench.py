@@ -330,6 +330,64 @@ class Stepper:
         L.check(self.lib.dpv_assemble_edges(self.h, P(self.x[0]), P(self.x[1]), P(self.x[2]),
                                             P(self.obj), L.stream_ptr()), "assemble_edges")
 
+    def fast_init(self, corr_items):
+        """Pre-built ctypes arguments for lm_step_fast (both state parities)."""
+        import ctypes as C
+        torch, w, P = self.torch, self.w, self.L.ptr
+        self.hp = torch.cuda.current_stream()
+        sp = lambda st: C.c_void_p(st.cuda_stream)
+        self.hp_p, self.side_p = sp(self.hp), sp(self.side)
+        g, (f0, f1) = w["gmap"], w["pyr"]
+        ii, jj = w["ii"].to(torch.int32).contiguous(), w["jj"].to(torch.int32).contiguous()
+        self._keep = (ii, jj)
+        self.corr_args = (P(g), int(g.shape[0]), P(f0), P(f1), int(f0.shape[0]), P(self.coords),
+                          P(ii), P(jj), self.Ec, int(g.shape[-1]), int(f0.shape[1]),
+                          int(f0.shape[2]), int(f1.shape[1]), int(f1.shape[2]), 2, 3,
+                          1 if g.dtype == torch.bfloat16 else 0, int(corr_items), P(self.cout),
+                          self.side_p)
+        self.fast = [None, None]
+        for par in range(2):
+            x, y = (self.x, self.y) if par == 0 else (self.y, self.x)
+            self.fast[par] = ([P(v) for v in x], [P(v) for v in y])
+        self.parity = 0
+        self.lam_c = C.c_double(self.lam)
+        self.csel_p = P(w["csel"])
+        self.misc = (P(self.dp), P(self.dd), P(self.status), P(self.obj))
+
+    def lm_step_fast(self):
+        """lm_step with pre-built arguments: ~8 library calls and 4 stream /
+        event operations per step, so the host stays well ahead of the device
+        (K1 on the low-priority side stream, the BA on the high-priority one)."""
+        lib, h, chk = self.lib, self.h, self.L.check
+        (xq, xt, xd), (yq, yt, yd) = self.fast[self.parity]
+        hs, ls = self.hp_p, self.side_p
+        dp, dd, status, obj = self.misc
+        r = lib.dpv_assemble_rest(h, xt, hs)
+        if r:
+            chk(r, "assemble_rest")
+        self.ev_fork.record(self.hp)
+        self.side.wait_event(self.ev_fork)
+        r = lib.dpv_reproject_coords_sel(h, xq, xt, xd, 0.25, self.csel_p, self.Ec,
+                                         self.corr_args[5], ls)
+        if r:
+            chk(r, "coords")
+        r = lib.dpv_corr_ex2(*self.corr_args)
+        if r:
+            chk(r, "corr")
+        self.ev_join.record(self.side)
+        r = lib.dpv_solve(h, self.lam_c, dp, dd, status, hs)
+        if r:
+            chk(r, "solve")
+        r = lib.dpv_apply_step(h, xq, xt, xd, dp, dd, yq, yt, yd, hs)
+        if r:
+            chk(r, "apply_step")
+        r = lib.dpv_assemble_edges(h, yq, yt, yd, obj, hs)
+        if r:
+            chk(r, "assemble_edges")
+        self.hp.wait_event(self.ev_join)
+        self.parity ^= 1
+        self.x, self.y = self.y, self.x
+
     def lm_step(self):
         """One LM iteration of the global BA as the native driver runs it
         (speculative assembly, ba.py:534-605 flow): the rest of the assembly at
@@ -378,15 +436,13 @@ class Stepper:
         torch.cuda.current_stream().wait_event(self.ev_join)
 
 
-def time_steps(fn, k, torch, clk=None):
+def time_steps(fn, k, torch):
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(k):
         fn()
-        if clk is not None:          # the device runs ahead of the launching thread
-            clk.sample()
     b.record()
     # wait with the GIL released so the clock sampler thread keeps polling
     # while the device runs (graph replays return immediately)
@@ -619,6 +675,13 @@ def run_ours(args):
     # cudaGraphInstantiateFlagUseNodePriority: measured 2.59 vs 2.40 ms eager)
     graph = None
     per_graph = 0
+    fast = None
+    if not work["sharded"] and not args.graph:
+        st.fast_init(args.corr_items)
+        fast = st.lm_step_fast
+        for _ in range(2):
+            fast()
+        torch.cuda.synchronize()
     if not work["sharded"] and args.graph and not args.no_graph and args.steps % 2 == 0:
         try:
             graph = torch.cuda.CUDAGraph()
@@ -640,7 +703,7 @@ def run_ours(args):
     if graph is not None:
         ms = time_steps(graph.replay, args.steps // 2, torch)
     else:
-        ms = time_steps(step_fn, args.steps, torch, clk)
+        ms = time_steps(fast or step_fn, args.steps, torch)
     clk.mark_end()
     clk.__exit__(None, None, None)
     launches = _lib.lib().dpv_launch_count() - launches0
@@ -760,8 +823,9 @@ def run_ours(args):
                    "W_blocks": int(work["info"].n_keys), "pairs": int(work["info"].n_pairs),
                    "feature_frames": work["n_feat_frames"],
                    "lm_attempt_per_step": 1,
-                   "step_kind": ("device-only LM iteration (" + ("replayed as a CUDA graph" if graph
-                                 is not None else "eager launches") + "): fixed lambda, "
+                   "step_kind": ("device-only LM iteration (" + (
+                                 "replayed as one CUDA graph" if graph is not None else
+                                 "eager launches") + "): fixed lambda, "
                                  "the candidate is always accepted, no host read-back; the native "
                                  "driver's per-iteration time (host accept test, lambda "
                                  "escalation) is global_ba.iteration_ms"),

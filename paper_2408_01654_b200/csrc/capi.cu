@@ -135,27 +135,33 @@ __global__ void k_scatter_depths(int64_t P, const int32_t* depth_patch, const do
 }
 
 // fixed-order sum of squares of two vectors -> out[0]
-__global__ void k_step_norm(int64_t n1, const double* a, int64_t n2, const double* b,
-                            double* out) {
+// The LM driver's per-attempt scalars in ONE pinned read-back:
+// out[1] = |(dp, dd)| (fixed-order reduction: 4 strided accumulators per
+// thread, xor-tree warp sums, warps summed in order), out[2] = the solve's
+// status flag, out[3] / out[4] = the assembly's gradient-max bits / inactive
+// count (scal[0], scal[6]); out[0] (the candidate objective) is written by the
+// edge pass.  One 1024-thread CTA: the norm of 6n + P values is ~5 us.
+__global__ void __launch_bounds__(1024) k_lm_scalars(int64_t n1, const double* a, int64_t n2,
+                                                     const double* b, const int32_t* status,
+                                                     const double* scal, double* out) {
     __shared__ double sh[32];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) s += a[i] * a[i];
-    double s2 = 0.0;
-    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) s2 += b[i] * b[i];
-    s = warp_sum(s);
-    s2 = warp_sum(s2);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-    __syncthreads();
-    double tot = 0.0;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sh[w];
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s2;
+    const int64_t T = blockDim.x;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    int u = 0;
+    for (int64_t i = threadIdx.x; i < n1; i += T, u = (u + 1) & 3) s[u] += a[i] * a[i];
+    for (int64_t i = threadIdx.x; i < n2; i += T, u = (u + 1) & 3) s[u] += b[i] * b[i];
+    double v = warp_sum((s[0] + s[1]) + (s[2] + s[3]));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t2 = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t2 += sh[w];
-        out[0] = sqrt(tot + t2);
+        double tot = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sh[w];
+        out[1] = sqrt(tot);
+        out[2] = (double)status[0];
+        // bit patterns (a count is not a double): integer copies
+        auto* bits = reinterpret_cast<unsigned long long*>(out);
+        bits[3] = reinterpret_cast<const unsigned long long*>(scal)[0];
+        bits[4] = reinterpret_cast<const unsigned long long*>(scal)[6];
     }
 }
 
@@ -658,7 +664,7 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     DPV_CUDA(cudaMemcpyAsync(wq, q, sizeof(double) * F * 4, cudaMemcpyDeviceToDevice, st));
     DPV_CUDA(cudaMemcpyAsync(wt, t, sizeof(double) * F * 3, cudaMemcpyDeviceToDevice, st));
     if (P) DPV_CUDA(cudaMemcpyAsync(wd, d, sizeof(double) * P, cudaMemcpyDeviceToDevice, st));
-    double* h = p->lm_host;  // pinned: [0] obj, [1] status, [2] step norm, [3] grad, [4] inact
+    double* h = p->lm_host;  // pinned: [0] obj, [1] step norm, [2] status, [3] grad, [4] inact
     double* dev_scalar = p->scal + 8;  // scal[8..15] LM scalars on the device
     // speculative assembly: every state's objective comes from its edge pass,
     // so the accepted candidate's pass is the next iteration's (ba.py:534-605
@@ -676,8 +682,6 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
     for (int it = 0; it < params->max_iterations; ++it) {
         const double tic = now_s();
         DPV_TRY(assemble_rest(p, wt, st));     // edge pass done when wq was evaluated
-        DPV_CUDA(cudaMemcpyAsync(h + 3, p->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
-        DPV_CUDA(cudaMemcpyAsync(h + 4, p->scal + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
         bool accepted = false, solved_once = false, singular = false;
         double grad = 0.0;
         int64_t inactive = 0;
@@ -687,14 +691,12 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
             DPV_TRY(solve(p, lam, p->lm_dp, p->lm_dd, status, st));
             DPV_TRY(apply_step(p, wq, wt, wd, p->lm_dp, p->lm_dd, p->lm_q, p->lm_t, p->lm_d, st));
             DPV_TRY(assemble_edges_pass(p, p->lm_q, p->lm_t, p->lm_d, dev_scalar, st));
-            k_step_norm<<<1, 256, 0, st>>>(6 * p->n, p->lm_dp, P, p->lm_dd, dev_scalar + 1);
+            k_lm_scalars<<<1, 1024, 0, st>>>(6 * p->n, p->lm_dp, P, p->lm_dd, status, p->scal,
+                                             dev_scalar);
             DPV_CHECK_LAUNCH();
-            DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
-            DPV_CUDA(cudaMemcpyAsync(h + 2, dev_scalar + 1, sizeof(double),
-                                     cudaMemcpyDeviceToHost, st));
-            int32_t sflag = 0;
-            DPV_CUDA(cudaMemcpyAsync(&sflag, status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            DPV_CUDA(cudaMemcpyAsync(h, dev_scalar, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
             DPV_CUDA(cudaStreamSynchronize(st));
+            const int32_t sflag = (int32_t)h[2];
             if (!grad_read) {
                 unsigned long long gb;
                 std::memcpy(&gb, h + 3, sizeof(gb));
@@ -722,7 +724,7 @@ int32_t dpv_lm_solve(dpv_problem* p, double* q, double* t, double* d,
                 std::swap(wt, p->lm_t);
                 std::swap(wd, p->lm_d);
                 obj = cand < obj ? cand : obj;
-                rep->step_norm = h[2];
+                rep->step_norm = h[1];
                 lam = lam * kShrink > 1e-12 ? lam * kShrink : 1e-12;
                 accepted = true;
                 break;
