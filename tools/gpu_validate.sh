@@ -10,4 +10,4 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-global --no-cpu > /dev/null 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spd_factor|k_assemble_edges_stg|k_key_blocks|k_incidences2|k_rows" -s 40 -c 8 -o gpurun_out/full python bench.py --steps 2 --warmup 3 --no-e2e --no-global --no-cpu --no-graph > /dev/null 2>&1; echo "ncu full rc=$?"
 # compute-sanitizer is closed on this GPU pool (profiles/sanitize_r02.txt); set SANITIZE=1 where it is allowed
-[ "${SANITIZE:-0}" = 1 ] && for t in memcheck racecheck synccheck; do timeout 1500 compute-sanitizer --tool $t --print-limit 10 python tools/sanitize_case.py > gpurun_out/san_$t.txt 2>&1; echo "$t: $(grep -E 'SUMMARY' gpurun_out/san_$t.txt)"; done
+if [ "${SANITIZE:-0}" = 1 ]; then for t in memcheck racecheck synccheck; do timeout 1500 compute-sanitizer --tool $t --print-limit 10 python tools/sanitize_case.py > gpurun_out/san_$t.txt 2>&1; echo "$t: $(grep -E 'SUMMARY' gpurun_out/san_$t.txt)"; done; fi
