@@ -38,8 +38,45 @@ void spd_plan_set_stream(SpdPlan* p, cudaStream_t st);
 int64_t spd_plan_bytes(const SpdPlan* p);
 void spd_plan_describe(const SpdPlan* p, int64_t* v);
 double spd_plan_flops(const SpdPlan* p);
+// S(lam) from the assembled system instead of precomputed blocks / rhs: the
+// scatter into the solver's storage forms each entry itself (no separate
+// reduced-system pass)
+struct SpdSysInput {
+    const double* pose = nullptr;       // (W, 36) pose blocks
+    const double* schur = nullptr;      // (W, 36) Schur blocks
+    const double* rhs_pose = nullptr;   // (n, 6)
+    const double* rhs_schur = nullptr;  // (n, 6)
+    const double* scal = nullptr;       // gauge pin (scal[1] flag, scal[2..4] u)
+    double lam = 0.0;
+};
 int32_t spd_factor_solve(SpdPlan* pl, const int32_t* ka, const int32_t* kb, const double* blocks,
-                         const double* rhs, double* dp, int32_t* status, cudaStream_t st);
+                         const double* rhs, double* dp, int32_t* status, cudaStream_t st,
+                         const SpdSysInput* sys = nullptr);
+
+// S(lam) block value at entry (i, j) of key w (ba.py:305-309)
+__device__ __forceinline__ double reduced_entry(const double* pose, const double* schur,
+                                                int64_t w, int idx, bool diag, double lam) {
+    double v = pose[w * 36 + idx] - schur[w * 36 + idx] / (1.0 + lam);
+    if (diag && (idx / 6 == idx % 6)) v += lam * pose[w * 36 + idx];
+    return v;
+}
+// ... plus the scale-gauge pin on the first free pose's block (ba.py:311-319)
+__device__ __forceinline__ double reduced_pinned_entry(const double* pose, const double* schur,
+                                                       const int32_t* ka, int64_t w, int idx,
+                                                       bool diag, double lam, const double* scal) {
+    double v = reduced_entry(pose, schur, w, idx, diag, lam);
+    if (w == 0 && scal[1] != 0.0 && diag && ka[0] == 0) {
+        const int i = idx / 6, j = idx % 6;
+        if (i < 3 && j < 3) {
+            double mx = 0.0;
+            for (int k = 0; k < 6; ++k)
+                mx = fmax(mx, fabs(reduced_entry(pose, schur, 0, k * 7, true, lam)));
+            const double mu = 1e6 * fmax(1.0, mx);
+            v += mu * scal[2 + i] * scal[2 + j];
+        }
+    }
+    return v;
+}
 }  // namespace dpv
 
 namespace dpv {
@@ -178,7 +215,6 @@ struct dpv_problem {
     std::thread plan_thread;
     dpv::SpdPlan* spd_pending = nullptr;
     int32_t plan_status = 0;
-    double* sblk = nullptr;        // (W, 36) S(lambda) blocks for the sparse solver
     int32_t* status = nullptr;     // (4) device flags
 
     // ---- LM scratch ------------------------------------------------------------

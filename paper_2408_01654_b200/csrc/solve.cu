@@ -22,13 +22,6 @@ namespace {
 
 constexpr int kSmallMax = 162;    // n <= 27 poses: single-CTA shared-memory solve
 
-// S(lam) block value at entry (i, j) of key w (ba.py:305-309)
-__device__ __forceinline__ double reduced_entry(const double* pose, const double* schur,
-                                                int64_t w, int idx, bool diag, double lam) {
-    double v = pose[w * 36 + idx] - schur[w * 36 + idx] / (1.0 + lam);
-    if (diag && (idx / 6 == idx % 6)) v += lam * pose[w * 36 + idx];
-    return v;
-}
 
 // ---------------------------------------------------------------------------
 // reduced system export (parity) -------------------------------------------
@@ -39,20 +32,8 @@ __global__ void k_reduced_blocks(int64_t W, const int32_t* ka, const int32_t* kb
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < W * 36;
          x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = x / 36;
-        const int idx = (int)(x % 36);
-        const bool diag = ka[w] == kb[w];
-        double v = reduced_entry(pose, schur, w, idx, diag, lam);
-        if (w == 0 && scal[1] != 0.0 && diag && ka[0] == 0) {
-            const int i = idx / 6, j = idx % 6;
-            if (i < 3 && j < 3) {
-                double mx = 0.0;
-                for (int k = 0; k < 6; ++k)
-                    mx = fmax(mx, fabs(reduced_entry(pose, schur, 0, k * 7, true, lam)));
-                const double mu = 1e6 * fmax(1.0, mx);
-                v += mu * scal[2 + i] * scal[2 + j];
-            }
-        }
-        out[x] = v;
+        out[x] = reduced_pinned_entry(pose, schur, ka, w, (int)(x % 36), ka[w] == kb[w], lam,
+                                      scal);
     }
 }
 
@@ -694,7 +675,6 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
                 p->spd_failed = 1;
                 return solve(p, lam, dp, dd, status, st);
             }
-            DPV_TRY(p->alloc(&p->sblk, p->W * 36));
         }
         if (!p->spd) {
             std::vector<int32_t> ka(p->W), kb(p->W);
@@ -711,10 +691,17 @@ int32_t solve(dpv_problem* p, double lam, double* dp, double* dd, int32_t* statu
                 p->spd_failed = 1;
                 return solve(p, lam, dp, dd, status, st);
             }
-            DPV_TRY(p->alloc(&p->sblk, p->W * 36));
         }
-        DPV_TRY(reduced_system(p, lam, p->sblk, p->red_rhs, nullptr, st));
-        DPV_TRY(spd_factor_solve(p->spd, p->key_a, p->key_b, p->sblk, p->red_rhs, dp, status, st));
+        // S(lam) and its rhs are formed by the scatter into the solver's storage
+        SpdSysInput sys;
+        sys.pose = p->pose_blocks;
+        sys.schur = p->schur_blocks;
+        sys.rhs_pose = p->rhs_pose;
+        sys.rhs_schur = p->rhs_schur;
+        sys.scal = p->scal;
+        sys.lam = lam;
+        DPV_TRY(spd_factor_solve(p->spd, p->key_a, p->key_b, nullptr, nullptr, dp, status, st,
+                                 &sys));
     } else {
         DPV_TRY(ensure_dense(p, N, st));
         DPV_TRY(dense_path(p, lam, N, *p->plan, p->perm_pos, dp, status, st));
