@@ -1080,12 +1080,30 @@ __global__ void __launch_bounds__(128) k_key_blocks_cta(
     }
 }
 
+// scale pin direction (ba.py:419-426)
+__device__ __forceinline__ void pin_direction(const double* t, int32_t first_free,
+                                              int32_t anchor, double* scal) {
+    double u[3];
+    for (int k = 0; k < 3; ++k) u[k] = t[3 * first_free + k] - (anchor >= 0 ? t[3 * anchor + k] : 0.0);
+    const double nrm = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    if (nrm > 1e-9) {
+        scal[1] = 1.0;
+        for (int k = 0; k < 3; ++k) scal[2 + k] = u[k] / nrm;
+    } else {
+        scal[1] = 0.0;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_var_rhs_cta(
     int64_t n, const int32_t* var_seg_ptr, const int32_t* var_seg, const double* seg_g,
     const int32_t* var_inc_ptr, const int32_t* inc_row, const double* inc_block,
     const double* cinv0, const double* rhs_depth, double* rhs_pose, double* rhs_schur,
-    unsigned long long* grad_bits) {
+    unsigned long long* grad_bits, const double* pin_t, int32_t pin_first, int32_t pin_anchor,
+    double* scal) {
     __shared__ double part[4][12];
+    // the scale-gauge pin (ba.py:311-319) rides along: one thread of CTA 0
+    // (pin_t == nullptr: the problem's scale is not degenerate)
+    if (pin_t && blockIdx.x == 0 && threadIdx.x == 0) pin_direction(pin_t, pin_first, pin_anchor, scal);
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
         double g[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};
@@ -1127,19 +1145,6 @@ __global__ void __launch_bounds__(128) k_var_rhs_cta(
             }
         }
         __syncthreads();
-    }
-}
-
-// scale pin direction (ba.py:419-426)
-__global__ void k_pin(const double* t, int32_t first_free, int32_t anchor, double* scal) {
-    double u[3];
-    for (int k = 0; k < 3; ++k) u[k] = t[3 * first_free + k] - (anchor >= 0 ? t[3 * anchor + k] : 0.0);
-    const double nrm = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-    if (nrm > 1e-9) {
-        scal[1] = 1.0;
-        for (int k = 0; k < 3; ++k) scal[2 + k] = u[k] / nrm;
-    } else {
-        scal[1] = 0.0;
     }
 }
 
@@ -1321,13 +1326,9 @@ int32_t assemble_rest(dpv_problem* p, const double* t, cudaStream_t st) {
         // against a warp per var)
         k_var_rhs_cta<<<(int)std::min<int64_t>(p->n, 65535), 128, 0, st>>>(
             p->n, p->var_seg_ptr, p->var_seg, p->seg_g, p->var_inc_ptr, p->inc_row,
-            p->inc_block, p->cinv0, p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits);
+            p->inc_block, p->cinv0, p->rhs_depth, p->rhs_pose, p->rhs_schur, grad_bits,
+            p->scale_degenerate ? t : nullptr, p->first, p->touched0, p->scal);
         DPV_CHECK_LAUNCH();
-        if (p->scale_degenerate) {
-            DPV_TSTART("pin", st);
-            k_pin<<<1, 1, 0, st>>>(t, p->first, p->touched0, p->scal);
-            DPV_CHECK_LAUNCH();
-        }
     }
     return DPV_OK;
 }
