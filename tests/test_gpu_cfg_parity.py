@@ -129,6 +129,10 @@ def test_lm_two_iterations(case):
     assert rep.initial_objective == pytest.approx(float(z["rep_initial"]), rel=1e-10)
     assert rep.final_objective == pytest.approx(float(z["rep_final"]), rel=1e-6)
     assert rep.final_damping == pytest.approx(float(z["rep_final_damping"]))
+    # the LM driver's packed per-attempt read-back (k_lm_scalars): the last
+    # accepted step's norm and the last assembly's gradient max
+    assert rep.step_norm == pytest.approx(float(z["rep_step_norm"]), rel=1e-5)
+    assert rep.gradient_norm == pytest.approx(float(z["rep_gradient_norm"]), rel=1e-5)
     q, t, d = prob.state()
     check(z, "after_q", q, 1e-7, 1e-9)
     check(z, "after_t", t, 1e-7, 1e-9)
