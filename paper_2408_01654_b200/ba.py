@@ -62,6 +62,24 @@ class _ForeignGraph:
             ref.patches[f][k] = ref.patches[f][k].with_inverse_depth(float(d[row]))
 
 
+_PINNED = {}
+
+
+def _pinned_copy(x):
+    """Device tensor -> numpy through a reused pinned host buffer (one
+    synchronising copy at full PCIe speed).  The returned array is a copy."""
+    torch = _torch()
+    key = (x.dtype, x.numel())
+    buf = _PINNED.get(key)
+    if buf is None:
+        if len(_PINNED) > 16:
+            _PINNED.clear()
+        buf = _PINNED[key] = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
+    buf.copy_(x.reshape(-1), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return buf.numpy().copy()
+
+
 class BAProblem:
     """Bundle adjustment problem over a contiguous free-pose range (ba.py:50-216).
 
@@ -200,11 +218,37 @@ class BAProblem:
     def state(self):
         return tuple(x.cpu().numpy() for x in self.device_state())
 
+    def _depth_rows_host(self):
+        """Graph patch id of every depth row (static per problem, cached) and,
+        when the rows are one contiguous ascending patch range, its start."""
+        if "depth_rows" not in self._cache:
+            dev = self.view("depth_patch")
+            n = int(dev.shape[0])
+            start, gid = None, None
+            if n:
+                # the rows are sorted unique patch ids (dpv_problem_create), so
+                # they form one range iff the endpoints are n - 1 apart
+                ends = dev[[0, n - 1]].cpu().numpy().astype(np.int64)
+                if ends[1] - ends[0] == n - 1:
+                    start = int(ends[0])
+            if start is None:
+                gid = dev.cpu().numpy().astype(np.int64)
+            self._cache["depth_rows"] = (n, gid, start)
+        return self._cache["depth_rows"]
+
     def write_back(self, q, t, d) -> None:
         torch = _torch()
-        q = q.cpu().numpy() if isinstance(q, torch.Tensor) else np.asarray(q, dtype=float)
-        t = t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t, dtype=float)
-        d = d.cpu().numpy() if isinstance(d, torch.Tensor) else np.asarray(d, dtype=float)
+        dev = [v for v in (q, t, d) if isinstance(v, torch.Tensor)]
+        if len(dev) == 3 and q.dtype == t.dtype == d.dtype == torch.float64:
+            # the whole state in one device->host copy (one synchronisation)
+            nq, nt = q.numel(), t.numel()
+            flat = _pinned_copy(torch.cat([q.reshape(-1), t.reshape(-1), d.reshape(-1)]))
+            q, t, d = (flat[:nq].reshape(tuple(q.shape)), flat[nq:nq + nt].reshape(tuple(t.shape)),
+                       flat[nq + nt:])
+        else:
+            q = q.cpu().numpy() if isinstance(q, torch.Tensor) else np.asarray(q, dtype=float)
+            t = t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t, dtype=float)
+            d = d.cpu().numpy() if isinstance(d, torch.Tensor) else np.asarray(d, dtype=float)
         if self._foreign is not None:
             self._foreign.write_back(self.first_free, self.last_free, q, t, self.depth_keys, d)
         g = self._g
@@ -213,11 +257,14 @@ class BAProblem:
         norm = np.linalg.norm(qf, axis=1, keepdims=True)
         g._q.view[sl] = np.where(np.abs(norm - 1.0) > 1e-12, qf / norm, qf)
         g._t.view[sl] = t[sl]
-        gid = self.view("depth_patch").cpu().numpy().astype(np.int64)
+        n_rows, gid, start = self._depth_rows_host()
         if np.any(~(d > 0)):
             from .errors import NonPositiveDepth
             raise NonPositiveDepth("patch inverse depth must be positive")
-        g._depth.view[gid] = d
+        if start is not None:
+            g._depth.view[start:start + n_rows] = d
+        else:
+            g._depth.view[gid] = d
         g._pose_ver += 1
         g._patch_ver += 1
 
