@@ -67,17 +67,19 @@ _PINNED = {}
 
 def _pinned_copy(x):
     """Device tensor -> numpy through a reused pinned host buffer (one
-    synchronising copy at full PCIe speed).  The returned array is a copy."""
+    synchronising copy at full PCIe speed).  One buffer per dtype, grown by
+    doubling, so problems of many sizes (window replicas) do not re-allocate
+    pinned memory.  The returned array is a copy."""
     torch = _torch()
-    key = (x.dtype, x.numel())
-    buf = _PINNED.get(key)
-    if buf is None:
-        if len(_PINNED) > 16:
-            _PINNED.clear()
-        buf = _PINNED[key] = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
-    buf.copy_(x.reshape(-1), non_blocking=True)
+    n = x.numel()
+    buf = _PINNED.get(x.dtype)
+    if buf is None or buf.numel() < n:
+        cap = max(n, 2 * (buf.numel() if buf is not None else 0), 1 << 16)
+        buf = _PINNED[x.dtype] = torch.empty(cap, dtype=x.dtype, pin_memory=True)
+    view = buf[:n]
+    view.copy_(x.reshape(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    return buf.numpy().copy()
+    return view.numpy().copy()
 
 
 class BAProblem:
